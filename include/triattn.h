@@ -1,0 +1,147 @@
+/* triattn.h -- C ABI v1 of the B200-native TriangleMix prefill-attention library.
+ *
+ * The library computes, for one prefill request (batch 1) and one attention
+ * layer, the masked softmax attention of PAPER.md section 2.1
+ *
+ *     O = Softmax( Q K^T * scale - c (1 - M') ) V ,   c -> +inf  (reading R3)
+ *
+ * with M' chosen per layer by TriangleMix (section 2.4):
+ *   dense layers    (layer <  tri_start):  M' = M, the causal mask;
+ *   triangle layers (layer >= tri_start):  M' = M - M^middle, i.e. for 0-based
+ *     query row i and key j <= i the pair is kept iff
+ *         j < sink  or  i - j < window  or  i >= N - last_q
+ *     (streaming section P:L120-131 + Last Q-K section; Middle Q-K
+ *      section P:L163-172 skipped; index reading R1 in DESIGN.md).
+ * The parameters are Algorithm 1's inputs (App. A.2):
+ * Q, K, V in R^{N x d_h}; N_sink, N_window, N_last.  Grouped-query attention
+ * ("generalizes naturally"): q head h reads kv head h / (Hq/Hkv)
+ * (reading R13).
+ *
+ * Conventions (every function):
+ *  - extern "C", never throws, never aborts, never prints.
+ *  - Tensors are caller-owned CUDA DEVICE memory; the library keeps no pointer
+ *    past the call.  Work is enqueued asynchronously on the caller's stream:
+ *    keep buffers alive until the stream reaches that point.
+ *  - Validation completes before anything is enqueued: on a non-OK return
+ *    nothing was launched and O / lse / workspace are untouched.
+ *  - Asynchronous device faults surface at the caller's next synchronisation.
+ *  - Degenerate triangle parameters (sink+window+last_q >= N, last_q >= N,
+ *    window >= N) are not errors: the result equals dense causal.
+ *  - The library owns only host/device caches (schedules, TMA descriptors),
+ *    keyed by device and problem signature, mutex-protected, freed by
+ *    ta_release_caches().  Calls from different threads/streams are safe.
+ *  - Same inputs + same SM count => bitwise-identical outputs.
+ */
+#ifndef TRIATTN_H_
+#define TRIATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TA_ABI_VERSION 1
+
+/* Same type as the CUDA runtime's cudaStream_t (a duplicate identical typedef is
+ * legal in C11/C++), so callers need no CUDA headers. NULL = legacy stream. */
+typedef struct CUstream_st *cudaStream_t;
+
+typedef enum {
+  TA_OK = 0,
+  TA_ERR_NULL_ARG = 1,       /* a required pointer is NULL                                      */
+  TA_ERR_EMPTY_SEQUENCE = 2, /* seq_len == 0                       (SPEC EmptySequence S:L56)   */
+  TA_ERR_SHAPE = 3,          /* heads < 1, Hq % Hkv != 0, seq_len < 0, stride too small
+                                (SPEC ShapeError S:L168)                                        */
+  TA_ERR_PARAMS = 4,         /* sink < 0, window < 1, last_q < 1, tri_start < 0, layer < 0
+                                (TriangleParams invariants S:L39-41; "last >= 1")       */
+  TA_ERR_UNSUPPORTED = 5,    /* head_dim not in {64,128}; Hq/Hkv > 128; seq_len >= 2^31;
+                                pointer not 16-byte aligned; stride*2 not a multiple of 16;
+                                device is not sm_100                                             */
+  TA_ERR_WORKSPACE = 6,      /* workspace NULL, too small, or not 256-byte aligned              */
+  TA_ERR_CUDA = 7            /* CUDA error while enqueuing; detail in ta_last_error()          */
+} ta_status;
+
+/* bf16 tensor view [heads][tokens][head_dim], element strides, head_dim stride 1.
+ * Head-major contiguous is stride_head = N*d, stride_token = d; token-major
+ * [N][H][d] is stride_head = d, stride_token = H*d. */
+typedef struct {
+  const void *data;
+  int64_t stride_head, stride_token;
+} ta_in_tensor;
+typedef struct {
+  void *data;
+  int64_t stride_head, stride_token;
+} ta_out_tensor;
+
+typedef struct {
+  ta_in_tensor q, k, v;  /* q: Hq heads; k, v: Hkv heads; bf16; device pointers, caller-owned */
+  ta_out_tensor o;       /* Hq heads, bf16, caller-owned, same shape as q                    */
+  float *lse;            /* optional [Hq][seq_len] fp32 natural-log log-sum-exp of the kept
+                            scores (Algorithm 1's "ln s + m"); NULL = not written     */
+  int64_t seq_len;       /* N >= 1 tokens (batch = 1 prefill, reading R16)                    */
+  int32_t num_q_heads;   /* Hq                                                                */
+  int32_t num_kv_heads;  /* Hkv; q head h reads kv head h / (Hq/Hkv)                          */
+  int32_t head_dim;      /* d in {64, 128}                                                    */
+  float softmax_scale;   /* <= 0 -> 1/sqrt(head_dim)  ("1/sqrt(d)")                   */
+} ta_problem;
+
+/* Triangle shape (Algorithm 1 "Input triangle shape"): si, sl, last. */
+typedef struct {
+  int32_t sink;   /* si >= 0 sink key columns  j < si */
+  int32_t window; /* sl >= 1 sliding-window keys  i - j < sl, incl. i */
+  int32_t last_q; /* last >= 1 final query rows  i >= N - last */
+} ta_triangle;
+
+/* Bytes of device workspace triangle_attn_prefill / dense_attn_prefill need
+ * (split-K partial outputs and their LSE for the Last-rows pass).
+ * tri == NULL -> dense.  Returns 0 on invalid arguments or when none is needed. */
+size_t ta_workspace_size(const ta_problem *p, const ta_triangle *tri);
+
+/* Triangle-shaped sparse causal attention of one deep layer,
+ * Algorithm 1 re-designed for sm_100a: a static block schedule
+ * of STREAM items (sink + sliding-window band per query tile, rows < N-last)
+ * and LASTQ split-K items (rows >= N-last, all causal keys in chunks), one
+ * persistent tcgen05/TMEM/TMA kernel, then an LSE merge kernel.
+ * ws: device workspace of >= ta_workspace_size(p, tri) bytes, 256-B aligned. */
+ta_status triangle_attn_prefill(const ta_problem *p, const ta_triangle *tri, void *ws,
+                                size_t ws_bytes, cudaStream_t stream);
+
+/* Dense causal attention of one shallow layer; the same kernel
+ * with DENSE items (keys [0, i] per row). ws may be NULL when
+ * ta_workspace_size(p, NULL) == 0. */
+ta_status dense_attn_prefill(const ta_problem *p, void *ws, size_t ws_bytes,
+                             cudaStream_t stream);
+
+/* Per-layer TriangleMix dispatch (reading R2): dense iff
+ * layer < tri_start, else triangle with *tri. */
+ta_status ta_layer_attn_prefill(int32_t layer, int32_t tri_start, const ta_problem *p,
+                                const ta_triangle *tri, void *ws, size_t ws_bytes,
+                                cudaStream_t stream);
+
+/* ---- introspection (host only; no GPU needed) ---------------------------- */
+
+/* Kept (i, j) pairs per head of the mask (tri == NULL -> dense causal).
+ * TA_ERR_EMPTY_SEQUENCE / TA_ERR_PARAMS as above. */
+ta_status ta_pair_count(int64_t seq_len, const ta_triangle *tri, int64_t *out_pairs_per_head);
+
+/* Serialise the static block schedule the kernel would run
+ * for (p, tri) on num_ctas persistent CTAs into host_buf.  Pointers inside *p
+ * are not dereferenced (they may be NULL).  *inout_bytes: capacity in, bytes
+ * needed/written out; host_buf == NULL or too small -> TA_ERR_WORKSPACE with
+ * *inout_bytes set to the size needed. */
+ta_status ta_schedule_export(const ta_problem *p, const ta_triangle *tri, int32_t num_ctas,
+                             void *host_buf, size_t *inout_bytes);
+
+const char *ta_status_str(ta_status s);
+/* Detail of this thread's last non-OK return ("" if none). */
+const char *ta_last_error(void);
+int32_t ta_abi_version(void);
+/* Free library-owned schedule/descriptor caches (device and host). */
+void ta_release_caches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRIATTN_H_ */

@@ -1,0 +1,242 @@
+"""B200-native TriangleMix prefill attention (arxiv 2507.21526) -- Python binding.
+
+Argument marshalling only: every step of the attention runs in the sm_100a
+kernels of ``libtriattn.so`` behind the C ABI declared in ``include/triattn.h``.
+PyTorch supplies device memory and the current CUDA stream; nothing here
+computes attention.  If the library is missing or the device is not a B200 the
+calls raise -- there is no CPU or PyTorch fallback.
+
+Function names follow the C ABI:
+
+    triangle_attn_prefill(q, k, v, sink=8, window=512, last_q=128)   # deep layers
+    dense_attn_prefill(q, k, v)                                      # shallow layers
+    layer_attn_prefill(layer, tri_start, q, k, v, ...)               # TriangleMix rule
+    pair_count(seq_len, sink, window, last_q) / schedule_export(...) # introspection
+
+q: [Hq][N][d] bf16 CUDA tensor view (any strides with unit d-stride), k/v:
+[Hkv][N][d]; q head h reads kv head h // (Hq/Hkv).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "TriattnError", "triangle_attn_prefill", "dense_attn_prefill", "layer_attn_prefill",
+    "workspace_size", "pair_count", "schedule_export", "abi_version", "release_caches",
+    "library_path", "STATUS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libtriattn.so")
+
+STATUS = {0: "TA_OK", 1: "TA_ERR_NULL_ARG", 2: "TA_ERR_EMPTY_SEQUENCE", 3: "TA_ERR_SHAPE",
+          4: "TA_ERR_PARAMS", 5: "TA_ERR_UNSUPPORTED", 6: "TA_ERR_WORKSPACE", 7: "TA_ERR_CUDA"}
+
+
+class TriattnError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{STATUS.get(status, status)}: {detail}")
+        self.status = status
+        self.detail = detail
+
+
+class _InTensor(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("stride_head", ctypes.c_int64),
+                ("stride_token", ctypes.c_int64)]
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("q", _InTensor), ("k", _InTensor), ("v", _InTensor), ("o", _InTensor),
+                ("lse", ctypes.c_void_p), ("seq_len", ctypes.c_int64),
+                ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("softmax_scale", ctypes.c_float)]
+
+
+class _Triangle(ctypes.Structure):
+    _fields_ = [("sink", ctypes.c_int32), ("window", ctypes.c_int32), ("last_q", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _SO
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO):
+        raise ImportError(f"{_SO} not built: run `python -m paper_2507_21526_b200.build` "
+                          "(there is no fallback path)")
+    lib = ctypes.CDLL(_SO)
+    P, Tp = ctypes.POINTER(_Problem), ctypes.POINTER(_Triangle)
+    vp, sz = ctypes.c_void_p, ctypes.c_size_t
+    lib.ta_workspace_size.argtypes = [P, Tp]
+    lib.ta_workspace_size.restype = sz
+    lib.triangle_attn_prefill.argtypes = [P, Tp, vp, sz, vp]
+    lib.triangle_attn_prefill.restype = ctypes.c_int
+    lib.dense_attn_prefill.argtypes = [P, vp, sz, vp]
+    lib.dense_attn_prefill.restype = ctypes.c_int
+    lib.ta_layer_attn_prefill.argtypes = [ctypes.c_int32, ctypes.c_int32, P, Tp, vp, sz, vp]
+    lib.ta_layer_attn_prefill.restype = ctypes.c_int
+    lib.ta_pair_count.argtypes = [ctypes.c_int64, Tp, ctypes.POINTER(ctypes.c_int64)]
+    lib.ta_pair_count.restype = ctypes.c_int
+    lib.ta_schedule_export.argtypes = [P, Tp, ctypes.c_int32, vp, ctypes.POINTER(sz)]
+    lib.ta_schedule_export.restype = ctypes.c_int
+    lib.ta_status_str.argtypes = [ctypes.c_int]
+    lib.ta_status_str.restype = ctypes.c_char_p
+    lib.ta_last_error.argtypes = []
+    lib.ta_last_error.restype = ctypes.c_char_p
+    lib.ta_abi_version.argtypes = []
+    lib.ta_abi_version.restype = ctypes.c_int32
+    lib.ta_release_caches.argtypes = []
+    lib.ta_release_caches.restype = None
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise TriattnError(status, _load().ta_last_error().decode())
+
+
+def _view(t):
+    return _InTensor(t.data_ptr(), t.stride(0), t.stride(1))
+
+
+def _problem(q, k, v, o, lse, scale):
+    p = _Problem()
+    p.q, p.k, p.v, p.o = _view(q), _view(k), _view(v), _view(o)
+    p.lse = lse.data_ptr() if lse is not None else None
+    p.seq_len = q.shape[1]
+    p.num_q_heads = q.shape[0]
+    p.num_kv_heads = k.shape[0]
+    p.head_dim = q.shape[2]
+    p.softmax_scale = float(scale)
+    return p
+
+
+def _check_tensors(q, k, v, o, lse):
+    import torch
+    for name, t in (("q", q), ("k", k), ("v", v), ("o", o)):
+        if t.dtype != torch.bfloat16 or t.dim() != 3 or not t.is_cuda or t.stride(2) != 1:
+            raise TriattnError(3, f"{name}: need a CUDA bf16 [heads][tokens][d] view, d-stride 1")
+    if k.shape != v.shape or q.shape[1:] != k.shape[1:] or o.shape != q.shape:
+        raise TriattnError(3, "q/k/v/o shapes disagree")
+    if lse is not None and (lse.dtype != torch.float32 or not lse.is_contiguous()
+                            or tuple(lse.shape) != (q.shape[0], q.shape[1])):
+        raise TriattnError(3, "lse must be contiguous fp32 [Hq][N]")
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(p, tri, device):
+    import torch
+    need = _load().ta_workspace_size(ctypes.byref(p), ctypes.byref(tri) if tri is not None else None)
+    if need == 0:
+        return None, 0
+    key = (device.index, need)
+    buf = _ws_cache.get(key)
+    if buf is None:
+        buf = torch.empty(need + 256, dtype=torch.uint8, device=device)
+        _ws_cache.clear()
+        _ws_cache[key] = buf
+    ptr = (buf.data_ptr() + 255) // 256 * 256
+    return ptr, need
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def triangle_attn_prefill(q, k, v, o=None, *, sink: int = 8, window: int = 512, last_q: int = 128,
+                          lse=None, scale: float = 0.0, stream=None):
+    """Triangle attention of one deep layer; returns o."""
+    import torch
+    if o is None:
+        o = torch.empty_like(q)
+    _check_tensors(q, k, v, o, lse)
+    p = _problem(q, k, v, o, lse, scale)
+    tri = _Triangle(sink, window, last_q)
+    ws, need = _workspace(p, tri, q.device)
+    _check(_load().triangle_attn_prefill(ctypes.byref(p), ctypes.byref(tri), ws, need,
+                                         _stream(stream)))
+    return o
+
+
+def dense_attn_prefill(q, k, v, o=None, *, lse=None, scale: float = 0.0, stream=None):
+    """Dense causal attention of one shallow layer; returns o."""
+    import torch
+    if o is None:
+        o = torch.empty_like(q)
+    _check_tensors(q, k, v, o, lse)
+    p = _problem(q, k, v, o, lse, scale)
+    ws, need = _workspace(p, None, q.device)
+    _check(_load().dense_attn_prefill(ctypes.byref(p), ws, need, _stream(stream)))
+    return o
+
+
+def layer_attn_prefill(layer: int, tri_start: int, q, k, v, o=None, *, sink: int = 8,
+                       window: int = 512, last_q: int = 128, lse=None, scale: float = 0.0,
+                       stream=None):
+    """TriangleMix per-layer dispatch: dense iff layer < tri_start (reading R2)."""
+    import torch
+    if o is None:
+        o = torch.empty_like(q)
+    _check_tensors(q, k, v, o, lse)
+    p = _problem(q, k, v, o, lse, scale)
+    tri = _Triangle(sink, window, last_q)
+    ws, need = _workspace(p, None if layer < tri_start else tri, q.device)
+    _check(_load().ta_layer_attn_prefill(layer, tri_start, ctypes.byref(p), ctypes.byref(tri), ws,
+                                         need, _stream(stream)))
+    return o
+
+
+def _shape_problem(seq_len, hq, hkv, d):
+    p = _Problem()
+    p.seq_len, p.num_q_heads, p.num_kv_heads, p.head_dim = seq_len, hq, hkv, d
+    return p
+
+
+def workspace_size(seq_len: int, hq: int, hkv: int, d: int, sink=8, window=512, last_q=128,
+                   dense: bool = False) -> int:
+    p = _shape_problem(seq_len, hq, hkv, d)
+    tri = None if dense else _Triangle(sink, window, last_q)
+    return int(_load().ta_workspace_size(ctypes.byref(p), ctypes.byref(tri) if tri else None))
+
+
+def pair_count(seq_len: int, sink=8, window=512, last_q=128, dense: bool = False) -> int:
+    out = ctypes.c_int64()
+    tri = None if dense else _Triangle(sink, window, last_q)
+    _check(_load().ta_pair_count(seq_len, ctypes.byref(tri) if tri else None, ctypes.byref(out)))
+    return out.value
+
+
+def schedule_export(seq_len: int, hq: int, hkv: int, d: int, num_ctas: int, sink=8, window=512,
+                    last_q=128, dense: bool = False) -> bytes:
+    p = _shape_problem(seq_len, hq, hkv, d)
+    tri = None if dense else _Triangle(sink, window, last_q)
+    tp = ctypes.byref(tri) if tri else None
+    n = ctypes.c_size_t(0)
+    lib = _load()
+    st = lib.ta_schedule_export(ctypes.byref(p), tp, num_ctas, None, ctypes.byref(n))
+    if st not in (0, 6):
+        _check(st)
+    buf = ctypes.create_string_buffer(n.value)
+    _check(lib.ta_schedule_export(ctypes.byref(p), tp, num_ctas, buf, ctypes.byref(n)))
+    return buf.raw[: n.value]
+
+
+def abi_version() -> int:
+    return int(_load().ta_abi_version())
+
+
+def release_caches() -> None:
+    _load().ta_release_caches()

@@ -1,0 +1,389 @@
+// api.cu -- the C ABI of include/triattn.h: validation, schedule/device caches,
+// TMA descriptor encoding and kernel launch.  No torch types anywhere.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "../../include/triattn.h"
+#include "kernel_params.h"
+#include "schedule.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ta_status fail(ta_status s, const std::string &msg) {
+  g_last_error = msg;
+  return s;
+}
+
+// ------------------------------------------------------------------ validation
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+ta_status validate_triangle(const ta_triangle *t) {
+  if (!t) return fail(TA_ERR_NULL_ARG, "triangle parameters are NULL");
+  if (t->sink < 0) return fail(TA_ERR_PARAMS, "sink < 0 (S:L39)");
+  if (t->window < 1) return fail(TA_ERR_PARAMS, "window < 1 (S:L39)");
+  if (t->last_q < 1) return fail(TA_ERR_PARAMS, "last_q < 1 (P:L161 'last >= 1')");
+  return TA_OK;
+}
+
+ta_status validate_shape(const ta_problem *p) {
+  if (!p) return fail(TA_ERR_NULL_ARG, "problem is NULL");
+  if (p->seq_len == 0) return fail(TA_ERR_EMPTY_SEQUENCE, "seq_len == 0 (S:L56)");
+  if (p->seq_len < 0) return fail(TA_ERR_SHAPE, "seq_len < 0");
+  if (p->num_q_heads < 1 || p->num_kv_heads < 1)
+    return fail(TA_ERR_SHAPE, "head counts must be >= 1");
+  if (p->num_q_heads % p->num_kv_heads != 0)
+    return fail(TA_ERR_SHAPE, "num_q_heads % num_kv_heads != 0");
+  if (p->head_dim != 64 && p->head_dim != 128)
+    return fail(TA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  if (p->num_q_heads / p->num_kv_heads > ta::kTileRows)
+    return fail(TA_ERR_UNSUPPORTED, "Hq/Hkv > 128");
+  if (p->seq_len >= (int64_t(1) << 31)) return fail(TA_ERR_UNSUPPORTED, "seq_len >= 2^31");
+  if (p->num_kv_heads > 65535) return fail(TA_ERR_UNSUPPORTED, "num_kv_heads > 65535");
+  return TA_OK;
+}
+
+ta_status validate_tensor(const char *name, const void *data, int64_t sh, int64_t st, int heads,
+                          int64_t n, int d) {
+  if (!data) return fail(TA_ERR_NULL_ARG, std::string(name) + ".data is NULL");
+  if (st < d || (heads > 1 && sh < 1) || sh < 0)
+    return fail(TA_ERR_SHAPE, std::string(name) + ": stride too small");
+  if (heads > 1 && n > 1) {
+    // views must not overlap: either head-major or token-major packing
+    bool head_major = sh >= n * st;
+    bool token_major = st >= (int64_t)heads * sh && sh >= d;
+    if (!head_major && !token_major)
+      return fail(TA_ERR_SHAPE, std::string(name) + ": overlapping head/token strides");
+  }
+  if (!aligned16(data)) return fail(TA_ERR_UNSUPPORTED, std::string(name) + ": not 16-byte aligned");
+  if ((st * 2) % 16 != 0 || (sh * 2) % 16 != 0)
+    return fail(TA_ERR_UNSUPPORTED, std::string(name) + ": stride*2 not a multiple of 16");
+  return TA_OK;
+}
+
+ta_status validate_problem(const ta_problem *p) {
+  ta_status s = validate_shape(p);
+  if (s != TA_OK) return s;
+  const int64_t n = p->seq_len;
+  const int d = p->head_dim;
+  if ((s = validate_tensor("q", p->q.data, p->q.stride_head, p->q.stride_token, p->num_q_heads, n, d)))
+    return s;
+  if ((s = validate_tensor("k", p->k.data, p->k.stride_head, p->k.stride_token, p->num_kv_heads, n, d)))
+    return s;
+  if ((s = validate_tensor("v", p->v.data, p->v.stride_head, p->v.stride_token, p->num_kv_heads, n, d)))
+    return s;
+  if ((s = validate_tensor("o", p->o.data, p->o.stride_head, p->o.stride_token, p->num_q_heads, n, d)))
+    return s;
+  return TA_OK;
+}
+
+// ------------------------------------------------------------------ caches
+struct DevSchedule {
+  ta::Geometry g;
+  ta::Item *d_items = nullptr;
+  uint32_t *d_offsets = nullptr;
+  int num_ctas = 0;
+};
+
+typedef std::tuple<int, int64_t, int, int, int, int, int, int, int, int> SchedKey;
+std::mutex g_mu;
+std::map<SchedKey, DevSchedule> g_sched;
+
+struct DeviceInfo {
+  int sms = 0, major = 0, minor = 0;
+};
+std::map<int, DeviceInfo> g_dev;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+
+ta_status device_info(int *dev, DeviceInfo *info) {
+  cudaError_t e = cudaGetDevice(dev);
+  if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_dev.find(*dev);
+  if (it == g_dev.end()) {
+    DeviceInfo di;
+    cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, *dev);
+    cudaDeviceGetAttribute(&di.major, cudaDevAttrComputeCapabilityMajor, *dev);
+    cudaDeviceGetAttribute(&di.minor, cudaDevAttrComputeCapabilityMinor, *dev);
+    it = g_dev.emplace(*dev, di).first;
+  }
+  *info = it->second;
+  if (info->major != 10 || info->minor != 0)
+    return fail(TA_ERR_UNSUPPORTED, "device is not sm_100 (B200)");
+  return TA_OK;
+}
+
+ta_status get_schedule(int dev, const ta::Geometry &g, int num_ctas, DevSchedule *out) {
+  SchedKey key(dev, g.n, g.hq, g.hkv, g.d, g.dense ? 1 : 0, g.si, g.sl, g.last, num_ctas);
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_sched.find(key);
+  if (it != g_sched.end()) {
+    *out = it->second;
+    return TA_OK;
+  }
+  ta::Schedule s = ta::build_schedule(g, num_ctas);
+  DevSchedule ds;
+  ds.g = s.g;
+  ds.num_ctas = num_ctas;
+  const size_t ib = std::max<size_t>(1, s.items.size()) * sizeof(ta::Item);
+  const size_t ob = s.offsets.size() * sizeof(uint32_t);
+  cudaError_t e = cudaMalloc(&ds.d_items, ib);
+  if (e == cudaSuccess) e = cudaMalloc(&ds.d_offsets, ob);
+  if (e == cudaSuccess && !s.items.empty())
+    e = cudaMemcpy(ds.d_items, s.items.data(), s.items.size() * sizeof(ta::Item), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ds.d_offsets, s.offsets.data(), ob, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(ds.d_items);
+    cudaFree(ds.d_offsets);
+    return fail(TA_ERR_CUDA, std::string("schedule upload: ") + cudaGetErrorString(e));
+  }
+  g_sched.emplace(key, ds);
+  *out = ds;
+  return TA_OK;
+}
+
+ta_status encode_map(CUtensorMap *m, const void *data, int64_t n, int heads, int d, int64_t sh,
+                     int64_t st, uint32_t box_rows, uint32_t box_heads) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_encode) {
+      void *fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+      if (e != cudaSuccess || !fn)
+        return fail(TA_ERR_CUDA, "cuTensorMapEncodeTiled entry point not found");
+      g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+    }
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)n, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {(cuuint64_t)(st * 2), (cuuint64_t)(sh * 2)};
+  if (heads == 1) strides[1] = (cuuint64_t)(st * 2) * (cuuint64_t)n;  // any legal value
+  cuuint32_t box[3] = {64u, box_rows, box_heads};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(data), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return TA_OK;
+}
+
+ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws, size_t ws_bytes,
+              cudaStream_t stream) {
+  ta_status s = validate_problem(p);
+  if (s != TA_OK) return s;
+  if (!dense && (s = validate_triangle(tri)) != TA_OK) return s;
+  int dev;
+  DeviceInfo di;
+  if ((s = device_info(&dev, &di)) != TA_OK) return s;
+  ta::Geometry g;
+  std::string err;
+  if (!ta::make_geometry(p->seq_len, p->num_q_heads, p->num_kv_heads, p->head_dim, dense,
+                         dense ? 0 : tri->sink, dense ? 1 : tri->window, dense ? 1 : tri->last_q,
+                         &g, &err))
+    return fail(TA_ERR_SHAPE, err);
+  ta::plan_chunks(&g, di.sms);
+  const size_t need = ta::workspace_bytes(g);
+  if (need > 0) {
+    if (!ws) return fail(TA_ERR_WORKSPACE, "workspace is NULL");
+    if (ws_bytes < need) return fail(TA_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+    if (reinterpret_cast<uintptr_t>(ws) & 255u) return fail(TA_ERR_WORKSPACE, "workspace not 256-byte aligned");
+  }
+  DevSchedule ds;
+  if ((s = get_schedule(dev, g, di.sms, &ds)) != TA_OK) return s;
+
+  ta::AttnParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  const int G = g.group, T = g.tile_tokens;
+  if ((s = encode_map(&prm.tm_q, p->q.data, g.n, g.hq, g.d, p->q.stride_head, p->q.stride_token, T, G)))
+    return s;
+  if ((s = encode_map(&prm.tm_k, p->k.data, g.n, g.hkv, g.d, p->k.stride_head, p->k.stride_token, 64, 1)))
+    return s;
+  if ((s = encode_map(&prm.tm_v, p->v.data, g.n, g.hkv, g.d, p->v.stride_head, p->v.stride_token, 64, 1)))
+    return s;
+  prm.o = p->o.data;
+  prm.o_sh = p->o.stride_head;
+  prm.o_st = p->o.stride_token;
+  prm.lse = p->lse;
+  if (need > 0) {
+    const int64_t slots = ta::num_partial_slots(ds.g);
+    const size_t o_bytes = ((size_t)slots * 2 * ta::kTileRows * g.d * 4 + 255) / 256 * 256;
+    prm.part_o = reinterpret_cast<float *>(ws);
+    prm.part_lse = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + o_bytes);
+  }
+  prm.items = ds.d_items;
+  prm.offsets = ds.d_offsets;
+  prm.n = (int)g.n;
+  prm.hq = g.hq;
+  prm.group = G;
+  prm.tile_tokens = T;
+  prm.pair_tokens = g.pair_tokens;
+  prm.si = g.si;
+  prm.sl = g.sl;
+  prm.last = g.last;
+  prm.dense = dense ? 1 : 0;
+  prm.p_last0 = (int)ds.g.p_last0;
+  prm.n_last_pairs = (int)ds.g.n_last_pairs;
+  prm.chunk_keys = ds.g.chunk_keys;
+  prm.s_max = ds.g.s_max;
+  const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / std::sqrt((float)g.d);
+  prm.scale = scale;
+  prm.scale_log2 = scale * 1.4426950408889634f;
+
+  cudaError_t e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
+  if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
+  if (!dense && ds.g.n_last_pairs > 0) {
+    e = ta::launch_merge(prm, g.d, g.hkv, stream);
+    if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
+  }
+  return TA_OK;
+}
+
+size_t ws_size(const ta_problem *p, const ta_triangle *tri) {
+  if (validate_shape(p) != TA_OK) return 0;
+  if (tri && validate_triangle(tri) != TA_OK) return 0;
+  ta::Geometry g;
+  if (!ta::make_geometry(p->seq_len, p->num_q_heads, p->num_kv_heads, p->head_dim, tri == nullptr,
+                         tri ? tri->sink : 0, tri ? tri->window : 1, tri ? tri->last_q : 1, &g, nullptr))
+    return 0;
+  int sms = 148;  // B200; used when no device is visible (host-only callers)
+  int dev;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+  } else {
+    cudaGetLastError();
+  }
+  ta::plan_chunks(&g, sms);
+  return ta::workspace_bytes(g);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ta_workspace_size(const ta_problem *p, const ta_triangle *tri) {
+  try {
+    return ws_size(p, tri);
+  } catch (...) {
+    return 0;
+  }
+}
+
+ta_status triangle_attn_prefill(const ta_problem *p, const ta_triangle *tri, void *ws,
+                                size_t ws_bytes, cudaStream_t stream) {
+  try {
+    if (!tri) return fail(TA_ERR_NULL_ARG, "triangle parameters are NULL");
+    return run(p, tri, false, ws, ws_bytes, stream);
+  } catch (const std::exception &ex) {
+    return fail(TA_ERR_CUDA, ex.what());
+  } catch (...) {
+    return fail(TA_ERR_CUDA, "unknown exception");
+  }
+}
+
+ta_status dense_attn_prefill(const ta_problem *p, void *ws, size_t ws_bytes, cudaStream_t stream) {
+  try {
+    return run(p, nullptr, true, ws, ws_bytes, stream);
+  } catch (const std::exception &ex) {
+    return fail(TA_ERR_CUDA, ex.what());
+  } catch (...) {
+    return fail(TA_ERR_CUDA, "unknown exception");
+  }
+}
+
+ta_status ta_layer_attn_prefill(int32_t layer, int32_t tri_start, const ta_problem *p,
+                                const ta_triangle *tri, void *ws, size_t ws_bytes,
+                                cudaStream_t stream) {
+  if (layer < 0) return fail(TA_ERR_PARAMS, "layer < 0");
+  if (tri_start < 0) return fail(TA_ERR_PARAMS, "tri_start < 0 (S:L40)");
+  // P:L255-269 with reading R2: layers [0, tri_start) dense, [tri_start, L) triangle.
+  if (layer < tri_start) return dense_attn_prefill(p, ws, ws_bytes, stream);
+  return triangle_attn_prefill(p, tri, ws, ws_bytes, stream);
+}
+
+ta_status ta_pair_count(int64_t seq_len, const ta_triangle *tri, int64_t *out) {
+  if (!out) return fail(TA_ERR_NULL_ARG, "out_pairs_per_head is NULL");
+  if (seq_len == 0) return fail(TA_ERR_EMPTY_SEQUENCE, "seq_len == 0 (S:L56)");
+  if (seq_len < 0) return fail(TA_ERR_SHAPE, "seq_len < 0");
+  const int64_t n = seq_len;
+  if (!tri) {
+    *out = n * (n + 1) / 2;
+    return TA_OK;
+  }
+  ta_status s = validate_triangle(tri);
+  if (s != TA_OK) return s;
+  // Row by row over the section definitions: rows i < N-last keep the
+  // streaming keys min(i+1, si+sl); rows i >= N-last keep all i+1 causal keys.
+  const int64_t w = (int64_t)tri->sink + tri->window;
+  const int64_t r = std::max<int64_t>(0, n - tri->last_q);
+  int64_t stream_pairs = r <= w ? r * (r + 1) / 2 : w * (w + 1) / 2 + (r - w) * w;
+  *out = stream_pairs + n * (n + 1) / 2 - r * (r + 1) / 2;
+  return TA_OK;
+}
+
+ta_status ta_schedule_export(const ta_problem *p, const ta_triangle *tri, int32_t num_ctas,
+                             void *host_buf, size_t *inout_bytes) {
+  try {
+    if (!inout_bytes) return fail(TA_ERR_NULL_ARG, "inout_bytes is NULL");
+    ta_status s = validate_shape(p);
+    if (s != TA_OK) return s;
+    if (tri && (s = validate_triangle(tri)) != TA_OK) return s;
+    if (num_ctas < 1) return fail(TA_ERR_PARAMS, "num_ctas < 1");
+    ta::Geometry g;
+    std::string err;
+    if (!ta::make_geometry(p->seq_len, p->num_q_heads, p->num_kv_heads, p->head_dim, tri == nullptr,
+                           tri ? tri->sink : 0, tri ? tri->window : 1, tri ? tri->last_q : 1, &g, &err))
+      return fail(TA_ERR_SHAPE, err);
+    std::vector<uint8_t> bytes = ta::serialize(ta::build_schedule(g, num_ctas));
+    const size_t cap = *inout_bytes;
+    *inout_bytes = bytes.size();
+    if (!host_buf || cap < bytes.size()) return fail(TA_ERR_WORKSPACE, "buffer too small");
+    std::memcpy(host_buf, bytes.data(), bytes.size());
+    return TA_OK;
+  } catch (...) {
+    return fail(TA_ERR_CUDA, "exception in ta_schedule_export");
+  }
+}
+
+const char *ta_status_str(ta_status s) {
+  switch (s) {
+    case TA_OK: return "TA_OK";
+    case TA_ERR_NULL_ARG: return "TA_ERR_NULL_ARG";
+    case TA_ERR_EMPTY_SEQUENCE: return "TA_ERR_EMPTY_SEQUENCE";
+    case TA_ERR_SHAPE: return "TA_ERR_SHAPE";
+    case TA_ERR_PARAMS: return "TA_ERR_PARAMS";
+    case TA_ERR_UNSUPPORTED: return "TA_ERR_UNSUPPORTED";
+    case TA_ERR_WORKSPACE: return "TA_ERR_WORKSPACE";
+    case TA_ERR_CUDA: return "TA_ERR_CUDA";
+  }
+  return "TA_ERR_UNKNOWN";
+}
+
+const char *ta_last_error(void) { return g_last_error.c_str(); }
+
+int32_t ta_abi_version(void) { return TA_ABI_VERSION; }
+
+void ta_release_caches(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto &kv : g_sched) {
+    cudaFree(kv.second.d_items);
+    cudaFree(kv.second.d_offsets);
+  }
+  g_sched.clear();
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// kernel_params.h -- parameter block shared by the host launcher and the sm_100a kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "schedule.h"
+
+namespace ta {
+
+// Passed by value as a __grid_constant__ kernel parameter; the TMA descriptors
+// must live in param space so cp.async.bulk.tensor can take their address.
+struct alignas(64) AttnParams {
+  CUtensorMap tm_q;  // Q [Hq][N][d]:   dims {d, N, Hq},  box {64, T, G}
+  CUtensorMap tm_k;  // K [Hkv][N][d]:  dims {d, N, Hkv}, box {64, 64, 1}
+  CUtensorMap tm_v;  // V, same as K
+  void *o;           // bf16 O [Hq][N][d] with element strides below
+  int64_t o_sh, o_st;
+  float *lse;        // optional [Hq][N]
+  float *part_o;     // split-K partials [slot][2*128 rows][d] fp32 (normalised O_c)
+  float *part_lse;   // [slot][2*128 rows] fp32 natural-log LSE_c
+  const Item *items;
+  const uint32_t *offsets;
+  int n, hq, group, tile_tokens, pair_tokens;
+  int si, sl, last, dense;
+  int p_last0, n_last_pairs, chunk_keys, s_max;
+  float scale_log2;  // softmax_scale * log2(e)
+  float scale;       // softmax_scale
+};
+
+// Launchers (kernels.cu). Return the CUDA error of the launch.
+cudaError_t launch_attention(const AttnParams &p, int head_dim, int num_ctas, cudaStream_t s);
+cudaError_t launch_merge(const AttnParams &p, int head_dim, int hkv, cudaStream_t s);
+size_t attention_smem_bytes(int head_dim);
+
+}  // namespace ta

@@ -1,0 +1,213 @@
+// schedule.cpp -- enumeration, costing and LPT assignment of the static block
+// schedule.  Pure host C++, no CUDA.
+#include "schedule.h"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <queue>
+
+namespace ta {
+
+static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+bool make_geometry(int64_t n, int hq, int hkv, int d, bool dense, int si, int sl, int last,
+                   Geometry *g, std::string *err) {
+  if (n < 1 || hq < 1 || hkv < 1 || hq % hkv != 0) {
+    if (err) *err = "bad shape";
+    return false;
+  }
+  Geometry r;
+  r.n = n;
+  r.hq = hq;
+  r.hkv = hkv;
+  r.d = d;
+  r.group = hq / hkv;
+  if (r.group > kTileRows) {
+    if (err) *err = "Hq/Hkv > 128 cannot be packed into one 128-row tile";
+    return false;
+  }
+  r.tile_tokens = kTileRows / r.group;
+  r.pair_tokens = kTilesPerItem * r.tile_tokens;
+  r.dense = dense;
+  r.si = dense ? 0 : si;
+  r.sl = dense ? 1 : sl;
+  r.last = dense ? 1 : last;
+  r.num_pairs = (n + r.pair_tokens - 1) / r.pair_tokens;
+  if (dense) {
+    r.p_last0 = r.num_pairs;
+    r.n_last_pairs = 0;
+  } else {
+    // Rows >= N - last are "last rows" (reading R1); a pair holding any of them is
+    // computed by the split-K pass over all of its causal keys (Algorithm 1).
+    int64_t last_start = std::max<int64_t>(0, n - last);
+    r.p_last0 = last_start / r.pair_tokens;
+    r.n_last_pairs = r.num_pairs - r.p_last0;
+  }
+  *g = r;
+  return true;
+}
+
+void pair_rows(const Geometry &g, int64_t p, int64_t *r0, int64_t *r1) {
+  *r0 = p * g.pair_tokens;
+  *r1 = std::min<int64_t>((p + 1) * g.pair_tokens, g.n) - 1;
+}
+
+static int64_t range_cost(int64_t kb, int64_t ke) {
+  int64_t c = 0;
+  for (int64_t k = kb; k < ke; k += kBlockKeys)
+    c += round_up(std::min<int64_t>(kBlockKeys, ke - k), kKeyGranule);
+  return c;
+}
+
+int64_t item_cost(const Geometry &g, const Item &it) {
+  int64_t c = kItemOverhead;
+  if (it.kind == kStream) {
+    int64_t r0, r1;
+    pair_rows(g, it.pair, &r0, &r1);
+    c += range_cost(0, std::min<int64_t>(g.si, r1 + 1));  // sink keys
+  }
+  c += range_cost(it.key_begin, it.key_end);
+  return c;
+}
+
+static Item make_item(ItemKind kind, int kvh, int64_t pair, int64_t kb, int64_t ke) {
+  Item it;
+  it.kind = kind;
+  it.pad = 0;
+  it.kv_head = (uint16_t)kvh;
+  it.pair = (uint32_t)pair;
+  it.key_begin = (uint32_t)kb;
+  it.key_end = (uint32_t)ke;
+  return it;
+}
+
+static Item stream_item(const Geometry &g, int kvh, int64_t p) {
+  int64_t r0, r1;
+  pair_rows(g, p, &r0, &r1);
+  // Sliding-window band relative to the tile (reading R5): keys [max(si, r0-sl+1), r1].
+  int64_t b0 = std::max<int64_t>(g.si, r0 - g.sl + 1);
+  int64_t b1 = r1 + 1;
+  if (b0 > b1) b0 = b1;
+  return make_item(kStream, kvh, p, b0, b1);
+}
+
+void plan_chunks(Geometry *g, int num_ctas) {
+  if (g->dense) {
+    g->chunk_keys = 0;
+    g->s_max = 0;
+    return;
+  }
+  int64_t ctot = 0;
+  for (int64_t p = 0; p < g->p_last0; ++p) ctot += item_cost(*g, stream_item(*g, 0, p));
+  for (int64_t p = g->p_last0; p < g->num_pairs; ++p) {
+    int64_t r0, r1;
+    pair_rows(*g, p, &r0, &r1);
+    ctot += item_cost(*g, make_item(kLastQ, 0, p, 0, r1 + 1));
+  }
+  ctot *= g->hkv;
+  int64_t target = ctot / (4 * (int64_t)std::max(1, num_ctas));
+  int64_t ck = 512;
+  while (ck * 2 <= target && ck * 2 <= 16384) ck *= 2;
+  g->chunk_keys = (int)ck;
+  g->s_max = (int)((g->n + ck - 1) / ck);
+}
+
+Schedule build_schedule(const Geometry &g0, int num_ctas) {
+  Schedule s;
+  s.g = g0;
+  plan_chunks(&s.g, num_ctas);
+  const Geometry &g = s.g;
+  s.num_ctas = num_ctas;
+
+  // Canonical order: LASTQ (kvh, pair, chunk), then STREAM or DENSE (kvh, pair).
+  std::vector<Item> canon;
+  if (!g.dense) {
+    for (int kvh = 0; kvh < g.hkv; ++kvh)
+      for (int64_t p = g.p_last0; p < g.num_pairs; ++p) {
+        int64_t r0, r1;
+        pair_rows(g, p, &r0, &r1);
+        for (int64_t kb = 0; kb < r1 + 1; kb += g.chunk_keys)
+          canon.push_back(make_item(kLastQ, kvh, p, kb, std::min<int64_t>(kb + g.chunk_keys, r1 + 1)));
+      }
+    for (int kvh = 0; kvh < g.hkv; ++kvh)
+      for (int64_t p = 0; p < g.p_last0; ++p) canon.push_back(stream_item(g, kvh, p));
+  } else {
+    for (int kvh = 0; kvh < g.hkv; ++kvh)
+      for (int64_t p = 0; p < g.num_pairs; ++p) {
+        int64_t r0, r1;
+        pair_rows(g, p, &r0, &r1);
+        canon.push_back(make_item(kDense, kvh, p, 0, r1 + 1));
+      }
+  }
+  const size_t ni = canon.size();
+  std::vector<int64_t> cost(ni);
+  for (size_t i = 0; i < ni; ++i) cost[i] = item_cost(g, canon[i]);
+  std::vector<uint32_t> order(ni);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+
+  // LPT: each item to the least-loaded CTA, ties to the lowest CTA id.
+  typedef std::pair<int64_t, int> LoadCta;
+  std::priority_queue<LoadCta, std::vector<LoadCta>, std::greater<LoadCta>> heap;
+  for (int c = 0; c < num_ctas; ++c) heap.push(LoadCta(0, c));
+  std::vector<std::vector<uint32_t>> per(num_ctas);
+  for (uint32_t idx : order) {
+    LoadCta top = heap.top();
+    heap.pop();
+    per[top.second].push_back(idx);
+    heap.push(LoadCta(top.first + cost[idx], top.second));
+  }
+  s.offsets.assign(num_ctas + 1, 0);
+  s.items.reserve(ni);
+  for (int c = 0; c < num_ctas; ++c) {
+    s.offsets[c] = (uint32_t)s.items.size();
+    for (uint32_t idx : per[c]) s.items.push_back(canon[idx]);
+  }
+  s.offsets[num_ctas] = (uint32_t)s.items.size();
+  return s;
+}
+
+std::vector<uint8_t> serialize(const Schedule &s) {
+  const Geometry &g = s.g;
+  uint32_t hdr[16] = {kScheduleMagic,
+                      kScheduleVersion,
+                      (uint32_t)(g.dense ? 1 : 0),
+                      (uint32_t)g.n,
+                      (uint32_t)g.hq,
+                      (uint32_t)g.hkv,
+                      (uint32_t)g.d,
+                      (uint32_t)g.si,
+                      (uint32_t)g.sl,
+                      (uint32_t)g.last,
+                      (uint32_t)g.tile_tokens,
+                      (uint32_t)kTilesPerItem,
+                      (uint32_t)g.chunk_keys,
+                      (uint32_t)s.num_ctas,
+                      (uint32_t)s.items.size(),
+                      (uint32_t)g.s_max};
+  std::vector<uint8_t> out(sizeof(hdr) + s.offsets.size() * 4 + s.items.size() * sizeof(Item));
+  uint8_t *w = out.data();
+  std::memcpy(w, hdr, sizeof(hdr));
+  w += sizeof(hdr);
+  std::memcpy(w, s.offsets.data(), s.offsets.size() * 4);
+  w += s.offsets.size() * 4;
+  if (!s.items.empty()) std::memcpy(w, s.items.data(), s.items.size() * sizeof(Item));
+  return out;
+}
+
+int64_t num_partial_slots(const Geometry &g) {
+  return g.dense ? 0 : (int64_t)g.hkv * g.n_last_pairs * g.s_max;
+}
+
+size_t workspace_bytes(const Geometry &g) {
+  int64_t slots = num_partial_slots(g);
+  if (slots == 0) return 0;
+  const int64_t rows = (int64_t)kTilesPerItem * kTileRows;
+  size_t o_bytes = (size_t)slots * rows * g.d * sizeof(float);
+  size_t lse_bytes = (size_t)slots * rows * sizeof(float);
+  return round_up((int64_t)o_bytes, 256) + round_up((int64_t)lse_bytes, 256);
+}
+
+}  // namespace ta

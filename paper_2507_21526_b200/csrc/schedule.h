@@ -1,0 +1,81 @@
+// schedule.h -- static block schedule of TriangleMix prefill attention (host side).
+//
+// Algorithm 1 (App. A.2) launches a static grid of
+// ceil((N-N_last)/B_M) + S*ceil(N_last/B_M) programs per head: streaming
+// programs for the upper rows and S split-K programs per last-row tile.  Here
+// the same static work is enumerated once on the host as 16-byte ITEMS, costed
+// in key columns and assigned to persistent CTAs by deterministic LPT
+// (DESIGN.md section 4 is the normative spec; oracle/schedule_ref.py is an
+// independent re-implementation of it used by the tests).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ta {
+
+enum ItemKind : uint8_t { kStream = 0, kLastQ = 1, kDense = 2 };
+
+// One unit of work: NQT consecutive packed Q tiles ("a pair") of one kv head and
+// a key range.  STREAM: [key_begin,key_end) is the sliding-window band, the sink
+// [0, min(si, r1+1)) is implicit.  LASTQ: one split-K chunk of [0, r1+1).
+// DENSE: [0, r1+1).
+struct Item {
+  uint8_t kind;
+  uint8_t pad;
+  uint16_t kv_head;
+  uint32_t pair;
+  uint32_t key_begin;
+  uint32_t key_end;
+};
+static_assert(sizeof(Item) == 16, "item is 16 bytes");
+
+constexpr int kTileRows = 128;      // tcgen05 M: packed rows per Q tile
+constexpr int kTilesPerItem = 2;    // Q tiles sharing one K/V stream (two softmax warpgroups)
+constexpr int kBlockKeys = 128;     // max keys per K/V block (tcgen05 N of QK^T)
+constexpr int kKeyGranule = 16;     // MMA N granularity for M=128
+constexpr int kItemOverhead = 64;   // LPT cost of an item beyond its key columns (epilogue)
+constexpr uint32_t kScheduleMagic = 0x43534154u;  // "TASC"
+constexpr uint32_t kScheduleVersion = 1;
+
+struct Geometry {
+  int64_t n = 0;
+  int hq = 0, hkv = 0, d = 0;
+  int group = 0;        // G = Hq / Hkv
+  int tile_tokens = 0;  // T = floor(128 / G) tokens per packed Q tile
+  int pair_tokens = 0;  // P = kTilesPerItem * T tokens per item
+  bool dense = false;
+  int si = 0, sl = 1, last = 1;
+  int64_t num_pairs = 0;     // ceil(N / P)
+  int64_t p_last0 = 0;       // first pair containing a row >= N - last (triangle)
+  int64_t n_last_pairs = 0;  // num_pairs - p_last0 (triangle), 0 for dense
+  int chunk_keys = 0;        // split-K chunk length for LASTQ items
+  int s_max = 0;             // max chunks per last pair = ceil(N / chunk_keys)
+};
+
+struct Schedule {
+  Geometry g;
+  int num_ctas = 0;
+  std::vector<uint32_t> offsets;  // num_ctas + 1
+  std::vector<Item> items;        // per-CTA lists, execution order
+};
+
+// Fills the geometry fields that do not depend on num_ctas. Returns false on bad input.
+// chunk_keys / s_max are set by plan_chunks() (they depend on num_ctas).
+bool make_geometry(int64_t n, int hq, int hkv, int d, bool dense, int si, int sl, int last,
+                   Geometry *g, std::string *err);
+// Row range [r0, r1] (tokens) of pair p, clipped to N.
+void pair_rows(const Geometry &g, int64_t p, int64_t *r0, int64_t *r1);
+// Sum of 16-rounded block widths over the item's key blocks + kItemOverhead.
+int64_t item_cost(const Geometry &g, const Item &it);
+// chunk_keys = largest power of two <= C_tot / (4 num_ctas), clamped to [512, 16384],
+// where C_tot is the total cost with every last pair as one unsplit LASTQ item.
+void plan_chunks(Geometry *g, int num_ctas);
+// plan_chunks + enumerate + LPT. num_ctas >= 1.
+Schedule build_schedule(const Geometry &g, int num_ctas);
+std::vector<uint8_t> serialize(const Schedule &s);
+// Partial-output slots (split-K workspace) and their byte size.
+int64_t num_partial_slots(const Geometry &g);
+size_t workspace_bytes(const Geometry &g);
+
+}  // namespace ta

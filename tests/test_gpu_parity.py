@@ -1,0 +1,179 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle.
+
+Tolerance (north_star, bf16 I/O): max-abs <= 2e-2 and mean-abs <= 2e-3 against the
+fp64 oracle evaluated on the same bf16 inputs.  Structural pins:
+V = 1 -> O = 1; Q = 0 with one-hot V -> exact count ratios within 1 bf16 ulp;
+window >= N -> dense; determinism.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2507_21526_b200 as ta
+import synth
+from oracle import cref, masks
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3
+
+
+def _run(q, k, v, si, sl, last, dense, lse=False, layout="head"):
+    dev = torch.device("cuda")
+    if layout == "token":
+        # token-major storage [N][H][d], passed as a [H][N][d] strided view
+        qd = q.permute(1, 0, 2).contiguous().to(dev).permute(1, 0, 2)
+        kd = k.permute(1, 0, 2).contiguous().to(dev).permute(1, 0, 2)
+        vd = v.permute(1, 0, 2).contiguous().to(dev).permute(1, 0, 2)
+        od = torch.empty((q.shape[1], q.shape[0], q.shape[2]), dtype=torch.bfloat16,
+                         device=dev).permute(1, 0, 2)
+    else:
+        qd, kd, vd = q.to(dev), k.to(dev), v.to(dev)
+        od = torch.empty_like(qd)
+    od.fill_(float("nan"))
+    ld = torch.full((q.shape[0], q.shape[1]), float("nan"), device=dev) if lse else None
+    if dense:
+        ta.dense_attn_prefill(qd, kd, vd, od, lse=ld)
+    else:
+        ta.triangle_attn_prefill(qd, kd, vd, od, sink=si, window=sl, last_q=last, lse=ld)
+    torch.cuda.synchronize()
+    return od.float().cpu(), (ld.cpu() if lse else None)
+
+
+def _compare(o_gpu, o_ref, what=""):
+    err = (o_gpu.double().numpy() - o_ref)
+    assert np.isfinite(o_gpu.numpy()).all(), f"{what}: non-finite output"
+    mx, mean = np.abs(err).max(), np.abs(err).mean()
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, f"{what}: max {mx:.3e} mean {mean:.3e}"
+    return mx, mean
+
+
+def _full_parity(hq, hkv, n, d, si, sl, last, dense, seed, dist="iid", layout="head", lse=False):
+    q, k, v = synth.make_qkv(hq, hkv, n, d, seed, dist, si)
+    o, l = _run(q, k, v, si, sl, last, dense, lse=lse, layout=layout)
+    o_ref, lse_ref, _ = cref.attention(q, k, v, si, sl, last, dense)
+    _compare(o, o_ref, f"hq{hq} hkv{hkv} n{n} d{d} dense{dense} {dist}")
+    if lse:
+        assert np.abs(l.double().numpy() - lse_ref).max() < 2e-3
+    return q, k, v, o
+
+
+# ---------------------------------------------------------------- C1 (configs[0])
+@pytest.mark.parametrize("dense", [False, True])
+def test_c1_full(dense):
+    c = synth.CONFIGS["C1"]
+    _full_parity(c.hq, c.hkv, c.n, c.d, c.si, c.sl, c.last, dense, 1000 * c.cid, lse=True)
+
+
+# ---------------------------------------------------------------- shapes and edges
+@pytest.mark.parametrize("n", [1, 7, 129, 1000, 4097])
+def test_llama_shape_small_n(n):
+    _full_parity(32, 8, n, 128, 8, 512, 128, False, seed=n)
+
+
+@pytest.mark.parametrize("n", [1, 130, 2049])
+def test_dense_small_n(n):
+    _full_parity(8, 2, n, 128, 0, 1, 1, True, seed=n + 1)
+
+
+@pytest.mark.parametrize("n", [700, 3001])
+def test_qwen_shape_g7(n):
+    _full_parity(28, 4, n, 128, 8, 512, 128, False, seed=n + 2)
+
+
+@pytest.mark.parametrize("dist", ["large", "sink"])
+def test_stress_distributions(dist):
+    _full_parity(8, 2, 2500, 128, 8, 512, 128, False, seed=77, dist=dist)
+
+
+def test_token_major_layout_and_lse():
+    _full_parity(8, 2, 1500, 128, 8, 512, 128, False, seed=5, layout="token", lse=True)
+
+
+def test_head_dim_64_gqa():
+    _full_parity(8, 2, 1800, 64, 8, 256, 64, False, seed=6)
+    _full_parity(8, 2, 900, 64, 0, 1, 1, True, seed=7)
+
+
+def test_odd_params():
+    # sink spans several blocks, window < tile, last not tile-aligned
+    _full_parity(4, 4, 3000, 128, 200, 40, 77, False, seed=8)
+    _full_parity(4, 1, 2000, 128, 0, 1, 1, False, seed=9)   # no sink, window 1, last 1
+    _full_parity(4, 2, 1200, 128, 3, 2000, 5, False, seed=10)  # window >= N
+
+
+# ---------------------------------------------------------------- structural pins
+def test_v_ones_gives_ones():
+    q, k, v = synth.make_qkv(32, 8, 3000, 128, seed=11, dist="ones_v")
+    o, _ = _run(q, k, v, 8, 512, 128, False)
+    assert (o - 1.0).abs().max().item() <= 2 ** -7
+
+
+def test_zero_q_onehot_v_exact_counts():
+    n, d, si, sl, last = 2000, 128, 8, 512, 128
+    q, k, v = synth.make_qkv(4, 1, n, d, seed=12, dist="zeroq_onehot")
+    o, _ = _run(q, k, v, si, sl, last, False)
+    o_ref, _, _ = cref.attention(q, k, v, si, sl, last, False)   # exact count ratios
+    ref_bf16 = torch.from_numpy(o_ref).to(torch.bfloat16).float()
+    ulp = torch.maximum(ref_bf16.abs() * 2 ** -7, torch.full_like(ref_bf16, 2 ** -133))
+    assert ((o - ref_bf16).abs() <= ulp).all()
+
+
+def test_window_ge_n_equals_dense_kernel():
+    q, k, v = synth.make_qkv(8, 2, 1500, 128, seed=13)
+    a, _ = _run(q, k, v, 4, 1500, 16, False)
+    b, _ = _run(q, k, v, 0, 1, 1, True)
+    assert (a - b).abs().max().item() < 1e-2
+
+
+def test_deterministic():
+    q, k, v = synth.make_qkv(32, 8, 5000, 128, seed=14)
+    a, _ = _run(q, k, v, 8, 512, 128, False)
+    b, _ = _run(q, k, v, 8, 512, 128, False)
+    assert torch.equal(a, b)
+
+
+def test_layer_dispatch():
+    q, k, v = synth.make_qkv(8, 2, 1500, 128, seed=15)
+    dev = torch.device("cuda")
+    qd, kd, vd = q.to(dev), k.to(dev), v.to(dev)
+    d_ = ta.dense_attn_prefill(qd, kd, vd)
+    t_ = ta.triangle_attn_prefill(qd, kd, vd)
+    assert torch.equal(ta.layer_attn_prefill(3, 16, qd, kd, vd), d_)
+    assert torch.equal(ta.layer_attn_prefill(16, 16, qd, kd, vd), t_)
+    assert torch.equal(ta.layer_attn_prefill(31, 16, qd, kd, vd), t_)
+
+
+# ---------------------------------------------------------------- errors on the GPU
+def test_errors_leave_output_untouched():
+    dev = torch.device("cuda")
+    q, k, v = (t.to(dev) for t in synth.make_qkv(8, 2, 256, 128, seed=16))
+    o = torch.full_like(q, 3.0)
+    with pytest.raises(ta.TriattnError) as e:
+        ta.triangle_attn_prefill(q, k, v, o, window=0)
+    assert e.value.status == 4
+    bad = torch.empty(8 * 256 * 128 + 1, dtype=torch.bfloat16, device=dev)[1:].view(8, 256, 128)
+    bad.copy_(q)
+    with pytest.raises(ta.TriattnError) as e:
+        ta.triangle_attn_prefill(q[:, :, :], k, v, bad)
+    assert e.value.status == 5
+    torch.cuda.synchronize()
+    assert (o == 3.0).all()
+
+
+# ---------------------------------------------------------------- full-size configs, sampled rows
+def _sample_rows(n, last, rng):
+    rows = set(range(0, 64)) | set(range(n - last - 64, n)) | set(range(n // 2 - 16, n // 2 + 16))
+    rows |= set(rng.choice(n, 256, replace=False).tolist())
+    return np.array(sorted(r for r in rows if 0 <= r < n))
+
+
+@pytest.mark.parametrize("name", ["C2"])
+def test_full_size_sampled_rows(name):
+    c = synth.CONFIGS[name]
+    q, k, v = synth.config_qkv(c, layer=16)
+    o, lse = _run(q, k, v, c.si, c.sl, c.last, False, lse=True)
+    rows = _sample_rows(c.n, c.last, np.random.default_rng(0))
+    o_ref, lse_ref, _ = cref.attention(q, k, v, c.si, c.sl, c.last, False, rows=rows)
+    _compare(o[:, rows], o_ref, name)
+    assert np.abs(lse[:, rows].double().numpy() - lse_ref).max() < 2e-3

@@ -1,0 +1,95 @@
+"""Static block schedule: byte identity with the independent enumerator, exact
+coverage of the mask by brute force, LPT balance (SURVEY 8(c) 'Schedule' pin)."""
+import random
+
+import numpy as np
+import pytest
+
+import paper_2507_21526_b200 as ta
+from oracle import masks, schedule_ref
+
+
+CASES = [
+    # n, hq, hkv, d, si, sl, last, dense, num_ctas
+    (512, 1, 1, 64, 4, 64, 64, False, 148),
+    (512, 1, 1, 64, 4, 64, 64, True, 148),
+    (4096, 32, 8, 128, 8, 512, 128, False, 148),
+    (4097, 28, 4, 128, 8, 512, 128, False, 148),
+    (1000, 8, 2, 128, 0, 100, 1, False, 7),
+    (129, 4, 4, 64, 16, 8, 200, False, 3),
+    (7, 2, 1, 128, 8, 512, 128, False, 148),
+    (1, 32, 8, 128, 8, 512, 128, False, 148),
+    (32768, 32, 8, 128, 8, 512, 128, False, 148),
+    (32768, 32, 8, 128, 8, 512, 128, True, 148),
+    (32768, 4, 1, 128, 8, 512, 128, False, 148),   # one kv-head shard (8 GPUs)
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_export_bytes_equal_independent_enumerator(case):
+    n, hq, hkv, d, si, sl, last, dense, nc = case
+    got = ta.schedule_export(n, hq, hkv, d, nc, si, sl, last, dense)
+    want = schedule_ref.serialize(n, hq, hkv, d, si, sl, last, dense, nc)
+    assert got == want
+
+
+def test_schedule_is_deterministic():
+    a = ta.schedule_export(20000, 32, 8, 128, 148)
+    b = ta.schedule_export(20000, 32, 8, 128, 148)
+    assert a == b
+
+
+def _block_keeps(geo, item, block, i):
+    """Keys of one block that the kernel keeps for row i (DESIGN.md section 4.3 rule)."""
+    kind, kvh, p, kb0, ke0 = item
+    btype, kb, w = block
+    si, sl, last, n = geo["si"], geo["sl"], geo["last"], geo["n"]
+    keys = range(kb, kb + w)
+    if kind == schedule_ref.STREAM:
+        if btype == "sink":
+            return [j for j in keys if j < si and j <= i]
+        return [j for j in keys if i - sl < j <= i]
+    if kind == schedule_ref.DENSE:
+        return [j for j in keys if j <= min(i, ke0 - 1)]
+    # LASTQ: triangle predicate inside the chunk
+    return [j for j in keys if kb0 <= j < ke0 and j <= i and (j < si or i - j < sl or i >= n - last)]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_items_cover_mask_exactly_once(seed):
+    rng = random.Random(seed)
+    n = rng.randint(1, 1500)
+    hkv = 1
+    hq = rng.choice([1, 2, 4, 7, 8])
+    si, sl, last = rng.randint(0, 40), rng.randint(1, 300), rng.randint(1, 300)
+    dense = rng.random() < 0.25
+    nc = rng.choice([1, 5, 148])
+    geo, ck, s_max, per, _ = schedule_ref.schedule(n, hq, hkv, 64, si, sl, last, dense, nc)
+    hits = np.zeros((n, n), dtype=np.int32)
+    for lst in per:
+        for it in lst:
+            r0, r1 = schedule_ref.rows(geo, it[2])
+            for blk in schedule_ref.item_blocks(geo, it):
+                assert blk[2] % 16 == 0 and 16 <= blk[2] <= 128
+                for i in range(r0, r1 + 1):
+                    for j in _block_keeps(geo, it, blk, i):
+                        hits[i, j] += 1
+    want = masks.mask_vectorised(n, si, sl, last, dense)
+    assert np.array_equal(hits, want.astype(np.int32))
+
+
+def test_lpt_balance_at_paper_configs():
+    for n, hq, hkv, nc, bound in [(32768, 32, 8, 148, 1.05), (131072, 32, 8, 148, 1.01),
+                                  (131072, 4, 1, 148, 1.05)]:
+        geo, ck, s_max, per, load = schedule_ref.schedule(n, hq, hkv, 128, 8, 512, 128, False, nc)
+        assert max(load) / (sum(load) / nc) <= bound, (n, hq, max(load) / (sum(load) / nc))
+
+
+def test_last_rows_go_through_split_k():
+    """Every row >= N-last belongs to a LASTQ pair (Algorithm 1 last-rows branch)."""
+    geo, ck, s_max, per, _ = schedule_ref.schedule(32768, 32, 8, 128, 8, 512, 128, False, 148)
+    last_pairs = {it[2] for lst in per for it in lst if it[0] == schedule_ref.LASTQ}
+    for i in range(32768 - 128, 32768):
+        assert i // geo["P"] in last_pairs
+    hdr, off, items = schedule_ref.parse(ta.schedule_export(32768, 32, 8, 128, 148))
+    assert hdr[0] == schedule_ref.MAGIC and hdr[12] == ck and hdr[15] == s_max
