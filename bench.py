@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""bench.py -- TriangleMix prefill attention on B200 (driver contract, one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N ...
+
+Workload: BASELINE.json configs[2], one deep (triangle) layer of
+Llama-3.1-8B attention (Hq=32, Hkv=8, d=128) at N=131072 tokens, si/sl/last =
+8/512/128, bf16 synthetic iid N(0,1) Q/K/V (synth recipe).  At N GPUs
+the layer is KV-head sharded (rank r owns kv heads [r*8/N, (r+1)*8/N) and their
+q heads) and each step ends with the NCCL all-gather of O, so the
+total work per step is fixed: "scaling": "strong".
+
+A step = one pass of the hot path over the layer: the persistent attention kernel
+(STREAM + LASTQ items), the LSE merge kernel, [the O all-gather].  value = kept-FLOP
+TFLOP/s of the whole layer (4*d*Hq*kept pairs, closed form) / max-over-ranks step
+time.  The dense causal layer (the speedup denominator) is timed in the same run.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also time C2/C4a/C4b (extra JSON key)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def kept_flops(c, hq_local, dense=False):
+    import paper_2507_21526_b200 as ta
+    pairs = ta.pair_count(c.n, dense=True) if dense else ta.pair_count(c.n, c.si, c.sl, c.last)
+    return 4 * c.d * hq_local * pairs
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get("bf16_tflops"), d.get("bf16_tflops_sustained"), d.get("hbm_gbs"), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes/launch of the attention kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_attn_summary.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline_run(c, q, k, v, seconds, dense=False):
+    """Time the fp64 C oracle on a bounded uniform row sample of the workload (all heads)."""
+    import numpy as np
+
+    from oracle import cref, masks  # noqa: F401  (bench's cpu_baseline leg only)
+    cores = len(os.sched_getaffinity(0))
+
+    def row_flops(rows):
+        tot = 0
+        for i in rows:
+            i = int(i)
+            if dense or i >= c.n - c.last:
+                cnt = i + 1
+            else:
+                cnt = min(i + 1, c.si + c.sl)
+            tot += cnt
+        return 4 * c.d * c.hq * tot
+
+    rng = np.random.default_rng(123)
+    probe = np.sort(rng.choice(c.n, 4, replace=False))
+    t0 = time.perf_counter()
+    cref.attention(q, k, v, c.si, c.sl, c.last, dense, rows=probe, threads=cores)
+    per_row = max((time.perf_counter() - t0) / len(probe), 1e-5)
+    nrows = int(max(8, min(c.n, seconds / per_row)))
+    rows = np.sort(rng.choice(c.n, nrows, replace=False))
+    t0 = time.perf_counter()
+    _, _, used = cref.attention(q, k, v, c.si, c.sl, c.last, dense, rows=rows, threads=cores)
+    dt = time.perf_counter() - t0
+    fl = row_flops(rows)
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": int(used), "kind": "oracle",
+            "sample": f"{nrows} uniformly sampled query rows x all {c.hq} q-heads of the "
+                      f"{c.name} {'dense' if dense else 'triangle'} layer (fp64 C oracle, "
+                      f"{dt:.1f} s wall)",
+            "seconds": dt}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    c = synth.CONFIGS[args.workload]
+    q, k, v = synth.config_qkv(c, layer=16)
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_baseline_run(c, q, k, v, per_step)
+        if s >= args.warmup:
+            vals.append(r)
+    tot_fl = sum(x["value"] * x["seconds"] for x in vals)
+    tot_s = sum(x["seconds"] for x in vals)
+    value = tot_fl / tot_s
+    line = {
+        "impl": "reference", "metric": "triangle-attn prefill kept-FLOP TFLOP/s (oracle)",
+        "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / len(vals), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {c.name} triangle layer si/sl/last="
+                               f"{c.si}/{c.sl}/{c.last}", "seq_len": c.n, "global_batch": 1},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": vals[0]["cores"],
+                         "kind": "oracle", "sample": vals[0]["sample"]},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    import paper_2507_21526_b200 as ta
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    c = synth.CONFIGS[args.workload]
+    if c.hkv % world != 0:
+        raise SystemExit(f"kv heads {c.hkv} not divisible by world size {world}")
+    hkv_l = c.hkv // world
+    g = c.hq // c.hkv
+    hq_l = hkv_l * g
+    q, k, v = synth.config_qkv(c, layer=16)      # CPU bf16, same recipe as the parity tests
+    qs = q[rank * hq_l:(rank + 1) * hq_l].contiguous()
+    ks = k[rank * hkv_l:(rank + 1) * hkv_l].contiguous()
+    vs = v[rank * hkv_l:(rank + 1) * hkv_l].contiguous()
+    qd, kd, vd = qs.to(dev), ks.to(dev), vs.to(dev)
+    od = torch.empty_like(qd)
+    o_full = torch.empty((c.hq, c.n, c.d), dtype=torch.bfloat16, device=dev) if world > 1 else None
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def layer(dense=False):
+        if dense:
+            ta.dense_attn_prefill(qd, kd, vd, od)
+        else:
+            ta.triangle_attn_prefill(qd, kd, vd, od, sink=c.si, window=c.sl, last_q=c.last)
+        if world > 1:
+            dist.all_gather_into_tensor(o_full, od)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def timed(steps, dense=False, profile=False):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        barrier()
+        if profile:
+            ta.profile_begin()
+        for s in range(steps):
+            flush.zero_()                 # L2 flush between timed iterations (> 126 MB L2)
+            evs[s][0].record(stream)
+            layer(dense)
+            evs[s][1].record(stream)
+        barrier()
+        prof = ta.profile_end() if profile else None
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        return max_over_ranks(ms / steps), prof
+
+    # ---- triangle layer: warmup + timed
+    for _ in range(args.warmup):
+        layer()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ms_tri, prof = timed(args.steps, profile=True)
+    clocks = sampler.stop()
+    attn_ms = max_over_ranks(prof["attn_ms"] / max(1, prof["attn_launches"]))
+    merge_ms = max_over_ranks(prof["merge_ms"] / max(1, prof["merge_launches"]))
+    gpu_launches = prof["attn_launches"] + prof["merge_launches"]
+
+    fl_layer = kept_flops(c, c.hq)
+    fl_rank = kept_flops(c, hq_l)
+    value = fl_layer / (ms_tri * 1e-3) / 1e12
+
+    # ---- dense layer (speedup denominator), same shard
+    dense_ms = None
+    if not args.no_dense:
+        layer(dense=True)
+        dense_ms, _ = timed(3, dense=True)
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        qh, kh, vh = qs.pin_memory(), ks.pin_memory(), vs.pin_memory()
+        oh = torch.empty(qs.shape, dtype=torch.bfloat16).pin_memory()
+        e_steps = min(args.steps, 3)
+
+        def e2e_step():
+            qd.copy_(qh, non_blocking=True)
+            kd.copy_(kh, non_blocking=True)
+            vd.copy_(vh, non_blocking=True)
+            layer()
+            oh.copy_(od, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps)
+        e2e = {"value": fl_layer / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int((qh.numel() + kh.numel() + vh.numel()) * 2),
+               "d2h_bytes_per_step": int(oh.numel() * 2)}
+
+    # ---- sweep of the other configs (1 GPU only; extra key)
+    sweep = None
+    if args.sweep and world == 1:
+        sweep = []
+        for name in ("C2", "C4a", "C4b"):
+            cc = synth.CONFIGS[name]
+            q2, k2, v2 = (t.to(dev) for t in synth.config_qkv(cc, layer=cc.tri_start))
+            o2 = torch.empty_like(q2)
+            res = {}
+            for dn in (False, True):
+                fn = (lambda: ta.dense_attn_prefill(q2, k2, v2, o2)) if dn else (
+                    lambda: ta.triangle_attn_prefill(q2, k2, v2, o2, sink=cc.si, window=cc.sl,
+                                                     last_q=cc.last))
+                for _ in range(3):
+                    fn()
+                reps = 3 if dn else 10
+                evs = []
+                barrier()
+                for _ in range(reps):
+                    flush.zero_()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    fn()
+                    b.record(stream)
+                    evs.append((a, b))
+                barrier()
+                res["dense_ms" if dn else "triangle_ms"] = sum(a.elapsed_time(b) for a, b in evs) / reps
+            res["triangle_tflops"] = kept_flops(cc, cc.hq) / (res["triangle_ms"] * 1e-3) / 1e12
+            res["dense_tflops"] = kept_flops(cc, cc.hq, True) / (res["dense_ms"] * 1e-3) / 1e12
+            res["speedup_vs_dense"] = res["dense_ms"] / res["triangle_ms"]
+            res["workload"] = cc.name
+            sweep.append(res)
+            del q2, k2, v2, o2
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_run(c, q, k, v, args.cpu_seconds)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        peak, peak_sus, hbm, src = measured_peaks()
+        achieved = fl_rank / (attn_ms * 1e-3) / 1e12
+        line = {
+            "metric": "triangle-attn prefill kept-FLOP TFLOP/s (ms/layer, speedup vs dense)",
+            "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_tri, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded iid N(0,1) bf16 Q/K/V, synth recipe)",
+            "config": {"workload": f"{args.workload}: {c.name}, one triangle (deep) layer, "
+                                   f"Hq={c.hq} Hkv={c.hkv} d={c.d} si/sl/last={c.si}/{c.sl}/{c.last}",
+                       "global_batch": 1, "seq_len": c.n,
+                       "parallelism": f"kv-head shard x{world}" + (" + NCCL all-gather of O" if world > 1 else ""),
+                       "l2": "flushed (512 MiB write) before every timed step; inputs 1.5 GB > L2"},
+            "ms_per_layer": ms_tri,
+            "dense_ms_per_layer": dense_ms,
+            "speedup_vs_dense": (dense_ms / ms_tri) if dense_ms else None,
+            "dense_tflops": (kept_flops(c, c.hq, True) / (dense_ms * 1e-3) / 1e12) if dense_ms else None,
+            "kernel_ms": {"attn": attn_ms, "merge": merge_ms},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
+                         "kernel": "attn_kernel<128> (persistent tcgen05 flash attention)",
+                         "algorithmic_flops_per_launch": fl_rank},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clocks,
+            "paper_context": "A100 Triton triangle 12/24/49 ms (3.7x/7.5x/15.3x vs FlashAttention) "
+                             "at 32K/64K/128K, P:L433-436; other hardware, context only",
+        }
+        if sweep is not None:
+            line["sweep"] = sweep
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,16 @@ int32_t ta_abi_version(void);
 /* Free library-owned schedule/descriptor caches (device and host). */
 void ta_release_caches(void);
 
+/* ---- kernel timing (used by bench.py) ------------------------------------ */
+/* While enabled, every prefill call records CUDA events on its stream around the
+ * attention kernel and around the merge kernel (library-owned events; the calls
+ * stay asynchronous).  ta_profile_end() synchronises those events, writes the
+ * summed device milliseconds and launch counts since ta_profile_begin(), and
+ * disables recording.  Any out-pointer may be NULL. */
+ta_status ta_profile_begin(void);
+ta_status ta_profile_end(double *attn_ms, int64_t *attn_launches, double *merge_ms,
+                         int64_t *merge_launches);
+
 #ifdef __cplusplus
 }
 #endif

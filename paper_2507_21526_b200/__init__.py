@@ -24,7 +24,7 @@ import os
 __all__ = [
     "TriattnError", "triangle_attn_prefill", "dense_attn_prefill", "layer_attn_prefill",
     "workspace_size", "pair_count", "schedule_export", "abi_version", "release_caches",
-    "library_path", "STATUS",
+    "library_path", "STATUS", "profile_begin", "profile_end",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -94,6 +94,11 @@ def _load():
     lib.ta_abi_version.restype = ctypes.c_int32
     lib.ta_release_caches.argtypes = []
     lib.ta_release_caches.restype = None
+    lib.ta_profile_begin.argtypes = []
+    lib.ta_profile_begin.restype = ctypes.c_int
+    lib.ta_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    lib.ta_profile_end.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -240,3 +245,17 @@ def abi_version() -> int:
 
 def release_caches() -> None:
     _load().ta_release_caches()
+
+
+def profile_begin() -> None:
+    """Start recording CUDA events around every attention / merge kernel launch."""
+    _check(_load().ta_profile_begin())
+
+
+def profile_end() -> dict:
+    """Stop recording; returns summed device ms and launch counts per kernel."""
+    a, m = ctypes.c_double(), ctypes.c_double()
+    na, nm = ctypes.c_int64(), ctypes.c_int64()
+    _check(_load().ta_profile_end(ctypes.byref(a), ctypes.byref(na), ctypes.byref(m), ctypes.byref(nm)))
+    return {"attn_ms": a.value, "attn_launches": na.value, "merge_ms": m.value,
+            "merge_launches": nm.value}

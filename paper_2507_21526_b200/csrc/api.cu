@@ -9,6 +9,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include "../../include/triattn.h"
 #include "kernel_params.h"
@@ -181,6 +182,26 @@ ta_status encode_map(CUtensorMap *m, const void *data, int64_t n, int heads, int
   return TA_OK;
 }
 
+// ------------------------------------------------------------------ timing
+struct Timing {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;  // recycled events
+  struct Rec { cudaEvent_t a0, a1, m1; };
+  std::vector<Rec> recs;
+};
+Timing g_timing;
+
+cudaEvent_t take_event() {
+  if (!g_timing.pool.empty()) {
+    cudaEvent_t e = g_timing.pool.back();
+    g_timing.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
 ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws, size_t ws_bytes,
               cudaStream_t stream) {
   ta_status s = validate_problem(p);
@@ -243,12 +264,26 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws,
   prm.scale = scale;
   prm.scale_log2 = scale * 1.4426950408889634f;
 
+  std::unique_lock<std::mutex> tlk(g_mu, std::defer_lock);
+  Timing::Rec rec{nullptr, nullptr, nullptr};
+  if (g_timing.on) {
+    tlk.lock();
+    rec.a0 = take_event();
+    rec.a1 = take_event();
+    cudaEventRecord(rec.a0, stream);
+  }
   cudaError_t e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
   if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
+  if (rec.a1) cudaEventRecord(rec.a1, stream);
   if (!dense && ds.g.n_last_pairs > 0) {
     e = ta::launch_merge(prm, g.d, g.hkv, stream);
     if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
+    if (rec.a0) {
+      rec.m1 = take_event();
+      cudaEventRecord(rec.m1, stream);
+    }
   }
+  if (rec.a0) g_timing.recs.push_back(rec);
   return TA_OK;
 }
 
@@ -376,6 +411,45 @@ const char *ta_status_str(ta_status s) {
 const char *ta_last_error(void) { return g_last_error.c_str(); }
 
 int32_t ta_abi_version(void) { return TA_ABI_VERSION; }
+
+ta_status ta_profile_begin(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_timing.on = true;
+  g_timing.recs.clear();
+  return TA_OK;
+}
+
+ta_status ta_profile_end(double *attn_ms, int64_t *attn_launches, double *merge_ms,
+                         int64_t *merge_launches) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  double a = 0, m = 0;
+  int64_t na = 0, nm = 0;
+  ta_status st = TA_OK;
+  for (auto &r : g_timing.recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.a1) != cudaSuccess || cudaEventSynchronize(r.a0) != cudaSuccess) {
+      st = fail(TA_ERR_CUDA, "event synchronize failed");
+    } else if (cudaEventElapsedTime(&t, r.a0, r.a1) == cudaSuccess) {
+      a += t;
+      ++na;
+    }
+    if (r.m1 && cudaEventSynchronize(r.m1) == cudaSuccess &&
+        cudaEventElapsedTime(&t, r.a1, r.m1) == cudaSuccess) {
+      m += t;
+      ++nm;
+    }
+    g_timing.pool.push_back(r.a0);
+    g_timing.pool.push_back(r.a1);
+    if (r.m1) g_timing.pool.push_back(r.m1);
+  }
+  g_timing.recs.clear();
+  g_timing.on = false;
+  if (attn_ms) *attn_ms = a;
+  if (attn_launches) *attn_launches = na;
+  if (merge_ms) *merge_ms = m;
+  if (merge_launches) *merge_launches = nm;
+  return st;
+}
 
 void ta_release_caches(void) {
   std::lock_guard<std::mutex> lk(g_mu);
