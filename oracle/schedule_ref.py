@@ -62,11 +62,22 @@ def rows(geo, p):
 
 
 def item_blocks(geo, it):
+    """Key blocks of an item: (type, first key, width in S columns).
+
+    type "fused": 16 sink columns (keys 0..15) followed by band keys from `first key`,
+    width = 16 + round16(min(112, band length)); used for STREAM items whose sink span
+    min(si, r1+1) is in 1..16.
+    """
     kind, kvh, p, kb, ke = it
     bl = []
     if kind == STREAM:
         r0, r1 = rows(geo, p)
-        bl += [("sink",) + b for b in blocks_of(0, min(geo["si"], r1 + 1))]
+        s_end = min(geo["si"], r1 + 1)
+        if 0 < s_end <= 16:
+            n0 = min(112, ke - kb)
+            bl.append(("fused", kb, 16 + _r16(n0)))
+            return bl + [("main",) + b for b in blocks_of(kb + 112, ke)]
+        bl += [("sink",) + b for b in blocks_of(0, s_end)]
     bl += [("main",) + b for b in blocks_of(kb, ke)]
     return bl
 

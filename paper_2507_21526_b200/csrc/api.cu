@@ -235,6 +235,12 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws,
     return s;
   if ((s = encode_map(&prm.tm_v, p->v.data, g.n, g.hkv, g.d, p->v.stride_head, p->v.stride_token, 64, 1)))
     return s;
+  if ((s = encode_map(&prm.tm_ks, p->k.data, g.n, g.hkv, g.d, p->k.stride_head, p->k.stride_token,
+                      ta::kSinkRows, 1)))
+    return s;
+  if ((s = encode_map(&prm.tm_vs, p->v.data, g.n, g.hkv, g.d, p->v.stride_head, p->v.stride_token,
+                      ta::kSinkRows, 1)))
+    return s;
   prm.o = p->o.data;
   prm.o_sh = p->o.stride_head;
   prm.o_st = p->o.stride_token;

@@ -21,6 +21,11 @@
 // every K/V block in shared memory.  TMEM (512 columns): S_A [0,128) S_B [128,256)
 // O_A [256,384) O_B [384,512); P (bf16) is written over its S columns and fed to the
 // PV MMA straight from TMEM.
+//
+// Sink fusion: when a STREAM item's sink span is <= 16 keys (si = 8 in the paper,
+// P:L295) the sink K/V rows are loaded with the Q tiles into a 16-row side buffer and
+// occupy S columns [0,16) of the first key block, whose remaining 112 columns hold the
+// start of the sliding-window band.
 #include <cuda_bf16.h>
 
 #include "kernel_params.h"
@@ -32,28 +37,45 @@ namespace {
 
 template <int D>
 struct Cfg {
-  static constexpr int kHalves = D / 64;               // 64-column (128 B) swizzle atoms
-  static constexpr int kHalfBytes = kTileRows * 128;   // one 64-col region of 128 rows
+  static constexpr int kHalves = D / 64;                 // 64-column (128 B) swizzle atoms
+  static constexpr int kHalfBytes = kTileRows * 128;     // one 64-col region of 128 rows
   static constexpr int kQTileBytes = kTileRows * D * 2;
-  static constexpr int kSlotBytes = kBlockKeys * D * 2;  // one K or V block
-  static constexpr int kStages = (D == 128) ? 5 : 10;
-  static constexpr int kBoxBytes = 64 * 128;          // TMA box: 64 rows x 64 cols bf16
+  static constexpr int kSinkHalfBytes = kSinkRows * 128;  // one 64-col region of 16 rows
+  static constexpr int kSinkBytes = kSinkRows * D * 2;
+  static constexpr int kSlotBytes = kBlockKeys * D * 2;   // one K or V block
+  static constexpr int kStages = (D == 128) ? 4 : 8;
+  static constexpr int kBoxBytes = 64 * 128;             // TMA box: 64 rows x 64 cols bf16
   static constexpr int kBarBytes = 1024;
-  static constexpr int kSmem = 1024 /*align slack*/ + 2 * kQTileBytes + kStages * kSlotBytes +
-                               kBarBytes;
+  static constexpr int kSmem = 1024 /*align slack*/ + 2 * kQTileBytes + 2 * kSinkBytes +
+                               kStages * kSlotBytes + kBarBytes;
 };
 
 constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
+constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
+// Bit k set: column pair k (of the 4 pairs in every 8 columns) uses the FMA-pipe exp2.
+constexpr int kPolyPairs = 0x1;            // 25% of the exponentials off the MUFU
 
 struct ItemInfo {
   int kind, kvh, pair;
   int kb0, ke0;   // item key range (band / chunk / causal)
   int r0, r1;     // token rows of the pair, clipped to N
-  int s_end, ns;  // sink keys [0, s_end) and their block count (STREAM only)
+  int fused;      // STREAM: sink (<= 16 keys) folded into block 0
+  int s_end, ns;  // STREAM unfused: sink keys [0, s_end) in ns blocks of their own
   int nb;         // total key blocks
 };
+
+struct Blk {
+  int kb;     // first key of the K/V slot rows
+  int nk;     // keys loaded into the slot (<= 128)
+  int sink;   // sink columns in front (0 or 16)
+  int ncols;  // total S columns (multiple of 16, <= 128)
+  int sinkblk;  // unfused sink block
+};
+
+__device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+__device__ __forceinline__ int round16(int a) { return (a + 15) & ~15; }
 
 __device__ __forceinline__ void item_info(const AttnParams &p, const Item &it, ItemInfo &f) {
   f.kind = it.kind;
@@ -63,33 +85,116 @@ __device__ __forceinline__ void item_info(const AttnParams &p, const Item &it, I
   f.ke0 = (int)it.key_end;
   f.r0 = f.pair * p.pair_tokens;
   f.r1 = min(f.r0 + p.pair_tokens, p.n) - 1;
+  f.fused = 0;
+  f.s_end = 0;
+  f.ns = 0;
+  const int len = f.ke0 - f.kb0;
   if (f.kind == kStream) {
     f.s_end = min(p.si, f.r1 + 1);
-    f.ns = (f.s_end + kBlockKeys - 1) / kBlockKeys;
-  } else {
-    f.s_end = 0;
-    f.ns = 0;
+    if (f.s_end > 0 && f.s_end <= kSinkRows) {
+      f.fused = 1;
+      const int first = kBlockKeys - kSinkRows;
+      f.nb = 1 + (len > first ? ceil_div(len - first, kBlockKeys) : 0);
+      return;
+    }
+    f.ns = ceil_div(f.s_end, kBlockKeys);
   }
-  f.nb = f.ns + (f.ke0 - f.kb0 + kBlockKeys - 1) / kBlockKeys;
+  f.nb = f.ns + ceil_div(len, kBlockKeys);
 }
 
-// Key block j of an item: first key kb, width n (multiple of 16, <= 128).
-__device__ __forceinline__ void block_range(const ItemInfo &f, int j, int &kb, int &n) {
-  int e;
-  if (j < f.ns) {
-    kb = j * kBlockKeys;
-    e = f.s_end;
+__device__ __forceinline__ Blk block_info(const ItemInfo &f, int j) {
+  Blk b;
+  b.sink = 0;
+  b.sinkblk = 0;
+  if (f.fused) {
+    if (j == 0) {
+      b.kb = f.kb0;
+      b.nk = min(kBlockKeys - kSinkRows, f.ke0 - f.kb0);
+      b.sink = kSinkRows;
+    } else {
+      b.kb = f.kb0 + (kBlockKeys - kSinkRows) + (j - 1) * kBlockKeys;
+      b.nk = min(kBlockKeys, f.ke0 - b.kb);
+    }
+  } else if (j < f.ns) {
+    b.kb = j * kBlockKeys;
+    b.nk = min(kBlockKeys, f.s_end - b.kb);
+    b.sinkblk = 1;
   } else {
-    kb = f.kb0 + (j - f.ns) * kBlockKeys;
-    e = f.ke0;
+    b.kb = f.kb0 + (j - f.ns) * kBlockKeys;
+    b.nk = min(kBlockKeys, f.ke0 - b.kb);
   }
-  n = min(kBlockKeys, e - kb);
-  n = (n + kKeyGranule - 1) & ~(kKeyGranule - 1);
+  b.ncols = b.sink + round16(b.nk);
+  return b;
 }
 
 __device__ __forceinline__ void ring_pos(uint32_t seq, int stages, uint32_t &slot, uint32_t &ph) {
   slot = seq % (uint32_t)stages;
   ph = (seq / (uint32_t)stages) & 1u;
+}
+
+// ---- packed fp32x2 helpers (FFMA2 / FADD2 on sm_100a)
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// 2^x for a pair on the FMA pipe (offloads the MUFU unit): x = j + f, j = rint(x),
+// f in [-1/2, 1/2], 2^f ~ 1 + c1 f + c2 f^2 + c3 f^3 (max rel. err 1.0e-4, far below the
+// bf16 rounding of P).  x is clamped to >= -127 so that x = -inf (a masked score) gives
+// exactly +0: p(0) = 1 and 1 * 2^-127 encodes as 0x00000000.
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float &y0, float &y1) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: rint via fp add
+  x0 = fmaxf(x0, -127.f);
+  x1 = fmaxf(x1, -127.f);
+  const uint64_t x = f2pack(x0, x1);
+  const uint64_t t = fadd2(x, f2pack(kMagic, kMagic));
+  const uint64_t r = fadd2(t, f2pack(-kMagic, -kMagic));
+  uint64_t f = fadd2(x, r ^ 0x8000000080000000ull);  // x - rint(x)
+  uint64_t pp = ffma2(f, f2pack(0.055008627f, 0.055008627f), f2pack(0.24221043f, 0.24221043f));
+  pp = ffma2(pp, f, f2pack(0.69328302f, 0.69328302f));
+  pp = ffma2(pp, f, f2pack(1.0f, 1.0f));
+  float p0, p1, t0, t1;
+  f2unpack(pp, p0, p1);
+  f2unpack(t, t0, t1);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
+__device__ __forceinline__ void tmem_ld32f(uint32_t taddr, float *f) {
+  uint32_t r[16];
+  ptx::tmem_ld16(taddr, r, 0);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(r[i]);
+  ptx::tmem_ld16(taddr + 16, r, 0);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[16 + i] = __uint_as_float(r[i]);
+}
+
+// Normalise a column interval; empty -> [kEmpty, kEmpty].
+__device__ __forceinline__ void norm_iv(int &lo, int &hi) {
+  if (lo > hi) {
+    lo = kEmpty;
+    hi = kEmpty;
+  }
 }
 
 template <int D>
@@ -98,8 +203,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-  uint8_t *sQ = smem;                             // [2][kQTileBytes]
-  uint8_t *sKV = smem + 2 * C::kQTileBytes;       // [kStages][kSlotBytes]
+  uint8_t *sQ = smem;                                   // [2][kQTileBytes]
+  uint8_t *sSinkK = smem + 2 * C::kQTileBytes;           // [halves][16 rows][128 B]
+  uint8_t *sSinkV = sSinkK + C::kSinkBytes;
+  uint8_t *sKV = sSinkV + C::kSinkBytes;                 // [kStages][kSlotBytes]
   uint64_t *bars = reinterpret_cast<uint64_t *>(sKV + C::kStages * C::kSlotBytes);
   uint64_t *kv_full = bars;
   uint64_t *kv_empty = bars + C::kStages;
@@ -143,7 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   const uint32_t it_beg = p.offsets[blockIdx.x];
   const uint32_t it_end = p.offsets[blockIdx.x + 1];
 
-  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;" ::: "memory");
+  // Register split (pool = 168 x 384): producer/MMA/alloc warpgroup 88, softmax 200.
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -153,19 +261,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       ptx::tma_prefetch_desc(&p.tm_v);
       uint32_t seq = 0, nitem = 0;
       const uint32_t q_bytes = 2u * C::kHalves * 128u * p.tile_tokens * p.group;
+      const uint32_t sink_bytes = 2u * C::kHalves * C::kSinkHalfBytes;
       for (uint32_t ii = it_beg; ii < it_end; ++ii, ++nitem) {
         ItemInfo f;
         item_info(p, p.items[ii], f);
         ptx::mbar_wait(q_empty, (nitem & 1u) ^ 1u);
-        ptx::mbar_arrive_expect_tx(q_full, q_bytes);
+        ptx::mbar_arrive_expect_tx(q_full, q_bytes + (f.fused ? sink_bytes : 0u));
         for (int x = 0; x < 2; ++x)
           for (int h = 0; h < C::kHalves; ++h)
             ptx::tma_load_3d(sQ + x * C::kQTileBytes + h * C::kHalfBytes, &p.tm_q, q_full, h * 64,
                              f.r0 + x * p.tile_tokens, f.kvh * p.group);
+        if (f.fused) {
+          for (int h = 0; h < C::kHalves; ++h) {
+            ptx::tma_load_3d(sSinkK + h * C::kSinkHalfBytes, &p.tm_ks, q_full, h * 64, 0, f.kvh);
+            ptx::tma_load_3d(sSinkV + h * C::kSinkHalfBytes, &p.tm_vs, q_full, h * 64, 0, f.kvh);
+          }
+        }
         for (int j = 0; j < f.nb; ++j) {
-          int kb, n;
-          block_range(f, j, kb, n);
-          const int nbox = (n + 63) / 64;
+          const Blk b = block_info(f, j);
+          const int nbox = ceil_div(b.nk, 64);
           for (int kv = 0; kv < 2; ++kv, ++seq) {
             uint32_t slot, ph;
             ring_pos(seq, C::kStages, slot, ph);
@@ -176,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             for (int h = 0; h < C::kHalves; ++h)
               for (int rb = 0; rb < nbox; ++rb)
                 ptx::tma_load_3d(dst + h * C::kHalfBytes + rb * C::kBoxBytes, tm, &kv_full[slot],
-                                 h * 64, kb + rb * 64, f.kvh);
+                                 h * 64, b.kb + rb * 64, f.kvh);
           }
         }
       }
@@ -188,26 +302,53 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
       const uint32_t qbase = ptx::smem_u32(sQ);
+      const uint32_t skbase = ptx::smem_u32(sSinkK);
+      const uint32_t svbase = ptx::smem_u32(sSinkV);
       const uint32_t kvbase = ptx::smem_u32(sKV);
       const uint32_t idesc_pv = ptx::idesc_bf16(128, D, 1);
+      const uint32_t idesc_sink = ptx::idesc_bf16(128, kSinkRows, 0);
       uint32_t seq = 0, nitem = 0;
       uint32_t pph[2] = {0, 0};
-      auto issue_qk = [&](int x, uint32_t kslot, int n) {
-        const uint32_t idesc = ptx::idesc_bf16(128, n, 0);
-        const uint32_t a0 = qbase + x * C::kQTileBytes;
-        const uint32_t b0 = kvbase + kslot * C::kSlotBytes;
-#pragma unroll
-        for (int s = 0; s < D / 16; ++s) {
-          const uint32_t off = (s / 4) * C::kHalfBytes + (s % 4) * 32;
-          ptx::mma_ss(tS[x], ptx::sdesc_sw128(a0 + off, 16, 1024),
-                      ptx::sdesc_sw128(b0 + off, 16, 1024), idesc, s > 0 ? 1u : 0u);
+      // Descriptors are built once; per MMA only the 14-bit start-address field moves
+      // (smem offsets < 256 KB, so adding (offset >> 4) to the descriptor never carries).
+      const uint64_t dq = ptx::sdesc_sw128(qbase, 16, 1024);
+      const uint64_t dsk = ptx::sdesc_sw128(skbase, 16, 1024);
+      const uint64_t dsv = ptx::sdesc_sw128(svbase, C::kSinkHalfBytes, 1024);
+      const uint64_t dkv = ptx::sdesc_sw128(kvbase, 16, 1024);
+      const uint64_t dkv_mn = ptx::sdesc_sw128(kvbase, C::kHalfBytes, 1024);
+      // S_x[:, cols] = Q_x K^T over the block (sink columns from the side buffer first).
+      auto issue_qk = [&](int x, uint32_t kslot, const Blk &b) {
+        const uint64_t a0 = dq + (uint64_t)((x * C::kQTileBytes) >> 4);
+        if (b.sink) {
+#pragma unroll 1
+          for (int s = 0; s < D / 16; ++s) {
+            const uint32_t kq = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
+            const uint32_t ks = ((s >> 2) * C::kSinkHalfBytes + (s & 3) * 32) >> 4;
+            ptx::mma_ss(tS[x], a0 + kq, dsk + ks, idesc_sink, s > 0 ? 1u : 0u);
+          }
+        }
+        const int nmain = b.ncols - b.sink;
+        if (nmain > 0) {
+          const uint32_t idesc = ptx::idesc_bf16(128, nmain, 0);
+          const uint64_t b0 = dkv + (uint64_t)((kslot * C::kSlotBytes) >> 4);
+#pragma unroll 1
+          for (int s = 0; s < D / 16; ++s) {
+            const uint32_t off = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
+            ptx::mma_ss(tS[x] + b.sink, a0 + off, b0 + off, idesc, s > 0 ? 1u : 0u);
+          }
         }
       };
-      auto issue_pv = [&](int x, uint32_t vslot, int n, bool acc) {
-        const uint32_t b0 = kvbase + vslot * C::kSlotBytes;
-        for (int s = 0; s < n / 16; ++s)
-          ptx::mma_ts(tO[x], tS[x] + s * 8, ptx::sdesc_sw128(b0 + s * 2048, C::kHalfBytes, 1024),
-                      idesc_pv, (acc || s > 0) ? 1u : 0u);
+      // O_x += P_x V over the block; P_x (bf16) lives in the S_x columns.
+      auto issue_pv = [&](int x, uint32_t vslot, const Blk &b, bool acc) {
+        if (b.sink) ptx::mma_ts(tO[x], tS[x], dsv, idesc_pv, acc ? 1u : 0u);
+        const uint64_t b0 = dkv_mn + (uint64_t)((vslot * C::kSlotBytes) >> 4);
+        const int ksteps = (b.ncols - b.sink) / 16;
+        const uint32_t pcol = tS[x] + b.sink / 2;
+        const uint32_t acc0 = (acc || b.sink) ? 1u : 0u;
+#pragma unroll 1
+        for (int s = 0; s < ksteps; ++s)
+          ptx::mma_ts(tO[x], pcol + s * 8, b0 + (uint64_t)(s * (2048 >> 4)), idesc_pv,
+                      (acc0 || s > 0) ? 1u : 0u);
       };
       for (uint32_t ii = it_beg; ii < it_end; ++ii, ++nitem) {
         ItemInfo f;
@@ -217,61 +358,60 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const uint32_t seq0 = seq;
         seq += 2u * f.nb;
         uint32_t kslot, kph, vslot, vph;
-        int kb, n;
-        block_range(f, 0, kb, n);
+        Blk b = block_info(f, 0);
         ring_pos(seq0, C::kStages, kslot, kph);
         ptx::mbar_wait(&kv_full[kslot], kph);
         ptx::tc_fence_after();
-        issue_qk(0, kslot, n);
+        issue_qk(0, kslot, b);
         ptx::tc_commit(&s_full[0]);
-        issue_qk(1, kslot, n);
+        issue_qk(1, kslot, b);
         ptx::tc_commit(&s_full[1]);
         ptx::tc_commit(&kv_empty[kslot]);
         if (f.nb == 1) ptx::tc_commit(q_empty);
         for (int j = 0; j < f.nb; ++j) {
-          const int nj = n;
           ring_pos(seq0 + 2 * j + 1, C::kStages, vslot, vph);
           ptx::mbar_wait(&kv_full[vslot], vph);
-          int kb1 = 0, n1 = 0;
-          uint32_t kslot1 = 0, kph1 = 0;
           const bool more = (j + 1 < f.nb);
+          Blk b1 = b;
+          uint32_t kslot1 = 0, kph1 = 0;
           if (more) {
-            block_range(f, j + 1, kb1, n1);
+            b1 = block_info(f, j + 1);
             ring_pos(seq0 + 2 * (j + 1), C::kStages, kslot1, kph1);
           }
           // ---- tile A: PV_A(j), then QK_A(j+1)
           ptx::mbar_wait(&p_ready[0], pph[0]);
           pph[0] ^= 1u;
           ptx::tc_fence_after();
-          issue_pv(0, vslot, nj, j > 0);
+          issue_pv(0, vslot, b, j > 0);
           if (!more) ptx::tc_commit(&o_full[0]);
           if (more) {
             ptx::mbar_wait(&kv_full[kslot1], kph1);
             ptx::tc_fence_after();
-            issue_qk(0, kslot1, n1);
+            issue_qk(0, kslot1, b1);
             ptx::tc_commit(&s_full[0]);
           }
           // ---- tile B: PV_B(j), then QK_B(j+1)
           ptx::mbar_wait(&p_ready[1], pph[1]);
           pph[1] ^= 1u;
           ptx::tc_fence_after();
-          issue_pv(1, vslot, nj, j > 0);
+          issue_pv(1, vslot, b, j > 0);
           if (!more) ptx::tc_commit(&o_full[1]);
           ptx::tc_commit(&kv_empty[vslot]);
           if (more) {
-            issue_qk(1, kslot1, n1);
+            issue_qk(1, kslot1, b1);
             ptx::tc_commit(&s_full[1]);
             ptx::tc_commit(&kv_empty[kslot1]);
             if (j + 2 == f.nb) ptx::tc_commit(q_empty);
           }
-          n = n1;
+          b = b1;
         }
       }
     }
     __syncwarp();
   } else if (warp >= 4) {
     // ===================== softmax / epilogue =====================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
+
     const int x = (warp - 4) / 4;   // Q tile of this warpgroup
     const int wq = warp % 4;        // TMEM lane quarter
     const int r = wq * 32 + lane;   // packed row = TMEM lane
@@ -282,86 +422,102 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     const bool row_in_tile = r < p.group * T;
     const int hoff = row_in_tile ? r / T : 0;
     const int toff = row_in_tile ? r % T : 0;
+    const float sc = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     for (uint32_t ii = it_beg; ii < it_end; ++ii) {
       ItemInfo f;
       item_info(p, p.items[ii], f);
       const int tok = f.r0 + x * T + toff;     // query row i of this thread
       const bool valid = row_in_tile && tok < p.n;
-      // Kept keys of row i inside one key block: [a_lo, a_hi] U [b_lo, b_hi]   (reading R1)
-      //   STREAM sink block : j < si, j <= i
-      //   STREAM band block : i - sl < j <= i  (band keys are >= si already)
-      //   LASTQ             : triangle predicate inside the chunk [kb0, ke0)
-      //   DENSE             : j <= i
-      // Sink and band blocks may cover the same key numbers (16-key rounding), so each
-      // block type keeps only its own section: no pair is counted twice.
       const bool last_row = tok >= p.n - p.last;
-      int la_lo, la_hi, lb_lo, lb_hi;  // LASTQ / DENSE intervals
-      if (f.kind == kLastQ) {
-        la_lo = f.kb0;
-        la_hi = last_row ? -1 : min(min(p.si, f.ke0) - 1, tok);
-        lb_lo = last_row ? f.kb0 : max(f.kb0, tok - p.sl + 1);
-        lb_hi = min(f.ke0 - 1, tok);
-      } else {
-        la_lo = 0;
-        la_hi = -1;
-        lb_lo = 0;
-        lb_hi = tok;
-      }
-      float m_run = -INFINITY;  // running max, log2 units of scaled scores
+      float m_run = -INFINITY;  // reference max, log2 units of scaled scores
       float l_run = 0.f;        // running sum of 2^(x - m_run)
       for (int j = 0; j < f.nb; ++j) {
-        int kb, n;
-        block_range(f, j, kb, n);
-        const int nch = n / 16;
+        const Blk b = block_info(f, j);
+        const int nch = (b.ncols + 31) >> 5;
+        // Kept columns of row i in this block: [a_lo, a_hi] U [b_lo, b_hi]   (reading R1)
+        //   STREAM fused block 0: sink cols j < si, j <= i, then band cols
+        //   STREAM sink block    : j < si, j <= i
+        //   STREAM band block    : i - sl < j <= i (band keys are >= si)
+        //   LASTQ                : triangle predicate within the chunk
+        //   DENSE                : j <= i
+        // Sink and band columns never cover the same key twice.
+        const int khi = b.kb + b.nk - 1;  // last key loaded in the slot
+        int a_lo = 0, a_hi = -1, b_lo, b_hi;
+        if (f.kind == kStream) {
+          if (b.sinkblk) {
+            b_lo = b.kb;
+            b_hi = min(min(p.si - 1, tok), khi);
+          } else {
+            b_lo = max(tok - p.sl + 1, b.kb);
+            b_hi = min(tok, khi);
+          }
+          if (b.sink) a_hi = min(p.si, tok + 1) - 1;
+        } else if (f.kind == kLastQ) {
+          if (!last_row) {
+            a_lo = max(f.kb0, b.kb);
+            a_hi = min(min(p.si - 1, tok), min(f.ke0 - 1, khi));
+          }
+          b_lo = max(b.kb, last_row ? f.kb0 : max(f.kb0, tok - p.sl + 1));
+          b_hi = min(min(f.ke0 - 1, tok), khi);
+        } else {
+          b_lo = b.kb;
+          b_hi = min(tok, khi);
+        }
+        // keys -> columns
+        if (f.kind != kStream || !b.sink) {
+          a_lo -= b.kb;
+          a_hi -= b.kb;
+        }
+        b_lo += b.sink - b.kb;
+        b_hi += b.sink - b.kb;
+        norm_iv(a_lo, a_hi);
+        norm_iv(b_lo, b_hi);
+        const int L = 32 * nch - 1;
+        const bool full = (b_lo <= 0 && b_hi >= L) || (a_lo <= 0 && a_hi >= L) ||
+                          (a_lo <= 0 && b_lo <= a_hi + 1 && b_hi >= L);
+        const bool warp_full = __all_sync(0xffffffffu, full);
+        const bool warp_two = __any_sync(0xffffffffu, a_lo != kEmpty);
+
         ptx::mbar_wait(&s_full[x], sph);
         sph ^= 1u;
         ptx::tc_fence_after();
         float s[128];
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c < nch) ptx::tmem_ld16f(tS + c * 16, &s[c * 16]);
+        tmem_ld32f(tS, s);
+        if (nch > 1) tmem_ld32f(tS + 32, s + 32);
+        if (nch > 2) tmem_ld32f(tS + 64, s + 64);
+        if (nch > 3) tmem_ld32f(tS + 96, s + 96);
         ptx::tmem_wait_ld();
-        int a_lo = la_lo, a_hi = la_hi, b_lo = lb_lo, b_hi = lb_hi;
-        if (f.kind == kStream) {
-          if (j < f.ns) {
-            a_lo = 0;
-            a_hi = min(p.si - 1, tok);
-            b_lo = 0;
-            b_hi = -1;
-          } else {
-            a_lo = 0;
-            a_hi = -1;
-            b_lo = tok - p.sl + 1;
-            b_hi = tok;
-          }
-        }
-        const bool full = ((kb >= b_lo) && (kb + n - 1 <= b_hi)) ||
-                          ((kb >= a_lo) && (kb + n - 1 <= a_hi));
-        const bool warp_full = __all_sync(0xffffffffu, full);
-        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+        if (!warp_full) {
+          const unsigned alen = (unsigned)(a_hi - a_lo), blen = (unsigned)(b_hi - b_lo);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (c < nch) {
+          for (int c = 0; c < 4; ++c) {
+            if (c < nch) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int idx = c * 16 + e;
-              float v = s[idx] * p.scale_log2;
-              if (!warp_full) {
-                const int key = kb + idx;
-                const bool kept = (key >= a_lo && key <= a_hi) || (key >= b_lo && key <= b_hi);
-                v = kept ? v : -INFINITY;
+              for (int e = 0; e < 32; ++e) {
+                const int col = c * 32 + e;
+                bool keep = (unsigned)(col - b_lo) <= blen;
+                if (warp_two) keep = keep || ((unsigned)(col - a_lo) <= alen);
+                s[col] = keep ? s[col] : -INFINITY;
               }
-              s[idx] = v;
-              if ((e & 3) == 0) mx0 = fmaxf(mx0, v);
-              else if ((e & 3) == 1) mx1 = fmaxf(mx1, v);
-              else if ((e & 3) == 2) mx2 = fmaxf(mx2, v);
-              else mx3 = fmaxf(mx3, v);
             }
           }
         }
-        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-        const float m_new = fmaxf(m_run, mx);
+        // raw row max (scale > 0 commutes with max)
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < nch) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) {
+              mx0 = max3(mx0, s[c * 32 + e], s[c * 32 + e + 1]);
+              mx1 = max3(mx1, s[c * 32 + e + 2], s[c * 32 + e + 3]);
+              mx2 = max3(mx2, s[c * 32 + e + 4], s[c * 32 + e + 5]);
+              mx3 = max3(mx3, s[c * 32 + e + 6], s[c * 32 + e + 7]);
+            }
+          }
+        }
+        const float m_new = fmaxf(m_run, max3(mx0, mx1, fmaxf(mx2, mx3)) * sc);
         const bool need = m_new > m_run + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
           const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
@@ -381,28 +537,40 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
         }
         const float ref = (m_run == -INFINITY) ? 0.f : m_run;
-        float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+        const uint64_t sc2 = f2pack(sc, sc);
+        const uint64_t nref2 = f2pack(-ref, -ref);
+        uint64_t l2a = 0, l2b = 0;  // packed partial row sums
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 4; ++c) {
           if (c < nch) {
-            uint32_t pk[8];
+            uint32_t pk[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float a = ptx::ex2(s[c * 16 + 2 * e] - ref);
-              const float b = ptx::ex2(s[c * 16 + 2 * e + 1] - ref);
-              if (e & 1) {
-                l2 += a;
-                l3 += b;
+            for (int e = 0; e < 32; e += 2) {
+              const uint64_t xx = ffma2(f2pack(s[c * 32 + e], s[c * 32 + e + 1]), sc2, nref2);
+              float x0, x1, p0, p1;
+              f2unpack(xx, x0, x1);
+              if ((kPolyPairs >> ((e >> 1) & 3)) & 1) {
+                // selected column pairs of every 8 on the FMA pipe, the rest on MUFU
+                exp2_poly2(x0, x1, p0, p1);
               } else {
-                l0 += a;
-                l1 += b;
+                p0 = ptx::ex2(x0);
+                p1 = ptx::ex2(x1);
               }
-              pk[e] = ptx::pack_bf16(a, b);
+              if (e & 2)
+                l2b = fadd2(l2b, f2pack(p0, p1));
+              else
+                l2a = fadd2(l2a, f2pack(p0, p1));
+              pk[e / 2] = ptx::pack_bf16(p0, p1);
             }
-            ptx::tmem_st8(tS + c * 8, pk);
+            ptx::tmem_st16(tS + c * 16, pk);
           }
         }
-        l_run += (l0 + l1) + (l2 + l3);
+        {
+          float a0, a1, b0, b1;
+          f2unpack(l2a, a0, a1);
+          f2unpack(l2b, b0, b1);
+          l_run += (a0 + a1) + (b0 + b1);
+        }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_ready[x]);

@@ -65,7 +65,16 @@ int64_t item_cost(const Geometry &g, const Item &it) {
   if (it.kind == kStream) {
     int64_t r0, r1;
     pair_rows(g, it.pair, &r0, &r1);
-    c += range_cost(0, std::min<int64_t>(g.si, r1 + 1));  // sink keys
+    const int64_t s_end = std::min<int64_t>(g.si, r1 + 1);  // sink keys
+    if (s_end > 0 && s_end <= kSinkRows) {
+      // fused: block 0 = 16 sink columns + up to 112 band keys, then 128-key band blocks
+      const int64_t first = kBlockKeys - kSinkRows;
+      const int64_t len = (int64_t)it.key_end - it.key_begin;
+      c += kSinkRows + round_up(std::min(first, len), kKeyGranule);
+      if (len > first) c += range_cost(it.key_begin + first, it.key_end);
+      return c;
+    }
+    c += range_cost(0, s_end);
   }
   c += range_cost(it.key_begin, it.key_end);
   return c;

@@ -34,6 +34,7 @@ constexpr int kTileRows = 128;      // tcgen05 M: packed rows per Q tile
 constexpr int kTilesPerItem = 2;    // Q tiles sharing one K/V stream (two softmax warpgroups)
 constexpr int kBlockKeys = 128;     // max keys per K/V block (tcgen05 N of QK^T)
 constexpr int kKeyGranule = 16;     // MMA N granularity for M=128
+constexpr int kSinkRows = 16;       // sink keys folded into a STREAM item's first block
 constexpr int kItemOverhead = 64;   // LPT cost of an item beyond its key columns (epilogue)
 constexpr uint32_t kScheduleMagic = 0x43534154u;  // "TASC"
 constexpr uint32_t kScheduleVersion = 1;

@@ -46,9 +46,13 @@ def _block_keeps(geo, item, block, i):
     si, sl, last, n = geo["si"], geo["sl"], geo["last"], geo["n"]
     keys = range(kb, kb + w)
     if kind == schedule_ref.STREAM:
+        if btype == "fused":
+            sink = [j for j in range(16) if j < si and j <= i]
+            band = [j for j in range(kb, min(kb + w - 16, ke0)) if i - sl < j <= i]
+            return sink + band
         if btype == "sink":
             return [j for j in keys if j < si and j <= i]
-        return [j for j in keys if i - sl < j <= i]
+        return [j for j in keys if i - sl < j <= i and j < ke0]
     if kind == schedule_ref.DENSE:
         return [j for j in keys if j <= min(i, ke0 - 1)]
     # LASTQ: triangle predicate inside the chunk
@@ -70,7 +74,7 @@ def test_items_cover_mask_exactly_once(seed):
         for it in lst:
             r0, r1 = schedule_ref.rows(geo, it[2])
             for blk in schedule_ref.item_blocks(geo, it):
-                assert blk[2] % 16 == 0 and 16 <= blk[2] <= 128
+                assert blk[2] % 16 == 0 and 16 <= blk[2] <= 128, blk
                 for i in range(r0, r1 + 1):
                     for j in _block_keeps(geo, it, blk, i):
                         hits[i, j] += 1
