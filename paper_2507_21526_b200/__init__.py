@@ -28,7 +28,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libtriattn.so")
+# TA_LIBRARY may point at the debug-timeline build (libtriattn_trace.so); same kernels.
+_SO = os.environ.get("TA_LIBRARY") or os.path.join(_HERE, "libtriattn.so")
 
 STATUS = {0: "TA_OK", 1: "TA_ERR_NULL_ARG", 2: "TA_ERR_EMPTY_SEQUENCE", 3: "TA_ERR_SHAPE",
           4: "TA_ERR_PARAMS", 5: "TA_ERR_UNSUPPORTED", 6: "TA_ERR_WORKSPACE", 7: "TA_ERR_CUDA"}

@@ -14,6 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtriattn.so")
+SO_TRACE = os.path.join(HERE, "libtriattn_trace.so")
 SOURCES = ["api.cu", "kernels.cu", "schedule.cpp"]
 HEADERS = ["ptx.cuh", "kernel_params.h", "schedule.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -30,20 +31,23 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """Compile libtriattn.so (or, with trace=True, the debug-timeline libtriattn_trace.so)."""
+    so = SO_TRACE if trace else SO
+    if not force and not trace and not _stale():
         return SO
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "--expt-relaxed-constexpr",
            "-I" + os.path.join(os.path.dirname(HERE), "include"),
-           "-o", SO + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES]
+           "-o", so + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES]
+    if trace:
+        cmd.insert(1, "-DTA_TRACE")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="--verbose" in sys.argv)
-    print(SO)
+    print(build(force=True, verbose="--verbose" in sys.argv, trace="--trace" in sys.argv))

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -182,6 +183,10 @@ ta_status encode_map(CUtensorMap *m, const void *data, int64_t n, int heads, int
   return TA_OK;
 }
 
+#ifdef TA_TRACE
+unsigned long long *g_trace_buf = nullptr;
+#endif
+
 // ------------------------------------------------------------------ timing
 struct Timing {
   bool on = false;
@@ -278,6 +283,17 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws,
     rec.a1 = take_event();
     cudaEventRecord(rec.a0, stream);
   }
+#ifdef TA_TRACE
+  {
+    static unsigned long long *tbuf = nullptr;
+    if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * 65536 * 4);
+    cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 65536 * 4, stream);
+    prm.trace = tbuf;
+    const char *e = getenv("TA_TRACE_CTA");
+    prm.trace_cta = e ? atoi(e) : 0;
+    g_trace_buf = tbuf;
+  }
+#endif
   cudaError_t e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
   if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
   if (rec.a1) cudaEventRecord(rec.a1, stream);
@@ -456,6 +472,16 @@ ta_status ta_profile_end(double *attn_ms, int64_t *attn_launches, double *merge_
   if (merge_launches) *merge_launches = nm;
   return st;
 }
+
+#ifdef TA_TRACE
+/* Debug build only: copy the last launch's timeline (4 x 65536 u64) to the host. */
+ta_status ta_debug_trace_read(void *host, size_t cap) {
+  if (!g_trace_buf) return TA_ERR_CUDA;
+  size_t n = sizeof(unsigned long long) * 65536 * 4;
+  cudaMemcpy(host, g_trace_buf, cap < n ? cap : n, cudaMemcpyDeviceToHost);
+  return TA_OK;
+}
+#endif
 
 void ta_release_caches(void) {
   std::lock_guard<std::mutex> lk(g_mu);

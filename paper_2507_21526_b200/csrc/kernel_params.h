@@ -29,6 +29,8 @@ struct alignas(64) AttnParams {
   int p_last0, n_last_pairs, chunk_keys, s_max;
   float scale_log2;  // softmax_scale * log2(e)
   float scale;       // softmax_scale
+  unsigned long long *trace;  // debug timeline (TA_TRACE builds only), else NULL
+  int trace_cta;
 };
 
 // Launchers (kernels.cu). Return the CUDA error of the launch.

@@ -35,6 +35,23 @@ namespace ta {
 
 namespace {
 
+#ifdef TA_TRACE
+// Debug timeline (builds with -DTA_TRACE only): clock64 stamps of one CTA's pipeline events.
+#define TRACE_AT(base, cnt, code, arg)                                                       \
+  do {                                                                                       \
+    if (p.trace && blockIdx.x == (unsigned)p.trace_cta && cnt < 65535)                       \
+      p.trace[(base) + (cnt)++] = ((uint64_t)(code) << 56) | ((uint64_t)((arg) & 0xff) << 48) | \
+                                  ((uint64_t)clock64() & 0xffffffffffffull);                  \
+  } while (0)
+#define TRACE_PR(code, arg) TRACE_AT(0, trc, code, arg)
+#define TRACE_MM(code, arg) TRACE_AT(65536, trc, code, arg)
+#define TRACE_SM(code, arg) do { if (lane == 0 && wq == 0) TRACE_AT(131072 + 65536 * x, trc, code, arg); } while (0)
+#else
+#define TRACE_PR(code, arg) do {} while (0)
+#define TRACE_MM(code, arg) do {} while (0)
+#define TRACE_SM(code, arg) do {} while (0)
+#endif
+
 template <int D>
 struct Cfg {
   static constexpr int kHalves = D / 64;                 // 64-column (128 B) swizzle atoms
@@ -55,7 +72,7 @@ constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 4 pairs in every 8 columns) uses the FMA-pipe exp2.
-constexpr int kPolyPairs = 0x1;            // 25% of the exponentials off the MUFU
+constexpr int kPolyPairs = 0x0;            // (0: all exponentials on the MUFU)
 
 struct ItemInfo {
   int kind, kvh, pair;
@@ -179,14 +196,19 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float &y0, float 
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
-__device__ __forceinline__ void tmem_ld32f(uint32_t taddr, float *f) {
-  uint32_t r[16];
-  ptx::tmem_ld16(taddr, r, 0);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(r[i]);
-  ptx::tmem_ld16(taddr + 16, r, 0);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) f[16 + i] = __uint_as_float(r[i]);
+__device__ __forceinline__ uint64_t u2pack(uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
+// Bits [lo, hi] of a 32-bit word (empty if hi < lo or outside [0, 31]).
+__device__ __forceinline__ uint32_t iv_bits(int lo, int hi) {
+  lo = max(lo, 0);
+  hi = min(hi, 31);
+  if (hi < lo) return 0u;
+  const uint32_t upto_hi = (hi == 31) ? 0xffffffffu : ((2u << hi) - 1u);
+  return upto_hi & ~((1u << lo) - 1u);
 }
 
 // Normalise a column interval; empty -> [kEmpty, kEmpty].
@@ -256,6 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
+#ifdef TA_TRACE
+      uint32_t trc = 0;
+#endif
       ptx::tma_prefetch_desc(&p.tm_q);
       ptx::tma_prefetch_desc(&p.tm_k);
       ptx::tma_prefetch_desc(&p.tm_v);
@@ -271,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           for (int h = 0; h < C::kHalves; ++h)
             ptx::tma_load_3d(sQ + x * C::kQTileBytes + h * C::kHalfBytes, &p.tm_q, q_full, h * 64,
                              f.r0 + x * p.tile_tokens, f.kvh * p.group);
+        TRACE_PR(1, nitem);
         if (f.fused) {
           for (int h = 0; h < C::kHalves; ++h) {
             ptx::tma_load_3d(sSinkK + h * C::kSinkHalfBytes, &p.tm_ks, q_full, h * 64, 0, f.kvh);
@@ -291,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
               for (int rb = 0; rb < nbox; ++rb)
                 ptx::tma_load_3d(dst + h * C::kHalfBytes + rb * C::kBoxBytes, tm, &kv_full[slot],
                                  h * 64, b.kb + rb * 64, f.kvh);
+            TRACE_PR(2 + kv, j);
           }
         }
       }
@@ -299,6 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
+#ifdef TA_TRACE
+      uint32_t trc = 0;
+#endif
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
       const uint32_t qbase = ptx::smem_u32(sQ);
@@ -355,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         item_info(p, p.items[ii], f);
         ptx::mbar_wait(q_full, nitem & 1u);
         ptx::tc_fence_after();
+        TRACE_MM(16, nitem);
         const uint32_t seq0 = seq;
         seq += 2u * f.nb;
         uint32_t kslot, kph, vslot, vph;
@@ -367,10 +398,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         issue_qk(1, kslot, b);
         ptx::tc_commit(&s_full[1]);
         ptx::tc_commit(&kv_empty[kslot]);
-        if (f.nb == 1) ptx::tc_commit(q_empty);
         for (int j = 0; j < f.nb; ++j) {
           ring_pos(seq0 + 2 * j + 1, C::kStages, vslot, vph);
           ptx::mbar_wait(&kv_full[vslot], vph);
+          TRACE_MM(17, j);
           const bool more = (j + 1 < f.nb);
           Blk b1 = b;
           uint32_t kslot1 = 0, kph1 = 0;
@@ -382,24 +413,33 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           ptx::mbar_wait(&p_ready[0], pph[0]);
           pph[0] ^= 1u;
           ptx::tc_fence_after();
+          TRACE_MM(10, j);
           issue_pv(0, vslot, b, j > 0);
+          TRACE_MM(11, j);
           if (!more) ptx::tc_commit(&o_full[0]);
           if (more) {
             ptx::mbar_wait(&kv_full[kslot1], kph1);
             ptx::tc_fence_after();
             issue_qk(0, kslot1, b1);
             ptx::tc_commit(&s_full[0]);
+            TRACE_MM(12, j);
           }
           // ---- tile B: PV_B(j), then QK_B(j+1)
           ptx::mbar_wait(&p_ready[1], pph[1]);
           pph[1] ^= 1u;
           ptx::tc_fence_after();
+          TRACE_MM(13, j);
           issue_pv(1, vslot, b, j > 0);
+          TRACE_MM(14, j);
           if (!more) ptx::tc_commit(&o_full[1]);
           ptx::tc_commit(&kv_empty[vslot]);
+          // Q tiles and the sink K/V side buffer are free once the item's last QK^T and
+          // its block-0 PV (which reads the sink V rows) have completed.
+          if (f.nb == 1) ptx::tc_commit(q_empty);
           if (more) {
             issue_qk(1, kslot1, b1);
             ptx::tc_commit(&s_full[1]);
+            TRACE_MM(15, j);
             ptx::tc_commit(&kv_empty[kslot1]);
             if (j + 2 == f.nb) ptx::tc_commit(q_empty);
           }
@@ -424,6 +464,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     const int toff = row_in_tile ? r % T : 0;
     const float sc = p.scale_log2;
     uint32_t sph = 0, oph = 0;
+#ifdef TA_TRACE
+    uint32_t trc = 0;
+#endif
     for (uint32_t ii = it_beg; ii < it_end; ++ii) {
       ItemInfo f;
       item_info(p, p.items[ii], f);
@@ -434,7 +477,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       float l_run = 0.f;        // running sum of 2^(x - m_run)
       for (int j = 0; j < f.nb; ++j) {
         const Blk b = block_info(f, j);
-        const int nch = (b.ncols + 31) >> 5;
         // Kept columns of row i in this block: [a_lo, a_hi] U [b_lo, b_hi]   (reading R1)
         //   STREAM fused block 0: sink cols j < si, j <= i, then band cols
         //   STREAM sink block    : j < si, j <= i
@@ -473,49 +515,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         b_hi += b.sink - b.kb;
         norm_iv(a_lo, a_hi);
         norm_iv(b_lo, b_hi);
-        const int L = 32 * nch - 1;
-        const bool full = (b_lo <= 0 && b_hi >= L) || (a_lo <= 0 && a_hi >= L) ||
-                          (a_lo <= 0 && b_lo <= a_hi + 1 && b_hi >= L);
+        // All 128 columns are processed every block (columns >= ncols are masked): no
+        // data-dependent branches inside the row loop.
+        const bool full = (b_lo <= 0 && b_hi >= 127) || (a_lo <= 0 && a_hi >= 127) ||
+                          (a_lo <= 0 && b_lo <= a_hi + 1 && b_hi >= 127);
         const bool warp_full = __all_sync(0xffffffffu, full);
-        const bool warp_two = __any_sync(0xffffffffu, a_lo != kEmpty);
 
         ptx::mbar_wait(&s_full[x], sph);
         sph ^= 1u;
         ptx::tc_fence_after();
-        float s[128];
-        tmem_ld32f(tS, s);
-        if (nch > 1) tmem_ld32f(tS + 32, s + 32);
-        if (nch > 2) tmem_ld32f(tS + 64, s + 64);
-        if (nch > 3) tmem_ld32f(tS + 96, s + 96);
+        TRACE_SM(20, j);
+        uint32_t s[128];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
         ptx::tmem_wait_ld();
         if (!warp_full) {
-          const unsigned alen = (unsigned)(a_hi - a_lo), blen = (unsigned)(b_hi - b_lo);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            if (c < nch) {
+            // kept-column bitmask of chunk c: [a_lo, a_hi] U [b_lo, b_hi] intersected with
+            // [32c, 32c + 31]
+            const uint32_t m32 = iv_bits(a_lo - 32 * c, a_hi - 32 * c) | iv_bits(b_lo - 32 * c, b_hi - 32 * c);
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                const int col = c * 32 + e;
-                bool keep = (unsigned)(col - b_lo) <= blen;
-                if (warp_two) keep = keep || ((unsigned)(col - a_lo) <= alen);
-                s[col] = keep ? s[col] : -INFINITY;
-              }
-            }
+            for (int e = 0; e < 32; ++e)
+              s[c * 32 + e] = (m32 & (1u << e)) ? s[c * 32 + e] : 0xff800000u;  // -inf
           }
         }
         // raw row max (scale > 0 commutes with max)
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < nch) {
-#pragma unroll
-            for (int e = 0; e < 32; e += 8) {
-              mx0 = max3(mx0, s[c * 32 + e], s[c * 32 + e + 1]);
-              mx1 = max3(mx1, s[c * 32 + e + 2], s[c * 32 + e + 3]);
-              mx2 = max3(mx2, s[c * 32 + e + 4], s[c * 32 + e + 5]);
-              mx3 = max3(mx3, s[c * 32 + e + 6], s[c * 32 + e + 7]);
-            }
-          }
+        for (int e = 0; e < 128; e += 8) {
+          mx0 = max3(mx0, __uint_as_float(s[e]), __uint_as_float(s[e + 1]));
+          mx1 = max3(mx1, __uint_as_float(s[e + 2]), __uint_as_float(s[e + 3]));
+          mx2 = max3(mx2, __uint_as_float(s[e + 4]), __uint_as_float(s[e + 5]));
+          mx3 = max3(mx3, __uint_as_float(s[e + 6]), __uint_as_float(s[e + 7]));
         }
         const float m_new = fmaxf(m_run, max3(mx0, mx1, fmaxf(mx2, mx3)) * sc);
         const bool need = m_new > m_run + kRescaleThreshold;
@@ -525,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           l_run *= alpha;
           if (j > 0) {
             // O_x holds exactly blocks < j: S_x(j) completing implies PV_x(j-1) completed.
-#pragma unroll
+#pragma unroll 1
             for (int c = 0; c < D / 16; ++c) {
               uint32_t o[16];
               ptx::tmem_ld16(tO + c * 16, o, 0);
@@ -539,46 +571,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const float ref = (m_run == -INFINITY) ? 0.f : m_run;
         const uint64_t sc2 = f2pack(sc, sc);
         const uint64_t nref2 = f2pack(-ref, -ref);
-        uint64_t l2a = 0, l2b = 0;  // packed partial row sums
+        float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < nch) {
-            uint32_t pk[16];
+        for (int c = 0; c < 8; ++c) {
+          uint32_t pk[8];
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const uint64_t xx = ffma2(f2pack(s[c * 32 + e], s[c * 32 + e + 1]), sc2, nref2);
-              float x0, x1, p0, p1;
-              f2unpack(xx, x0, x1);
-              if ((kPolyPairs >> ((e >> 1) & 3)) & 1) {
-                // selected column pairs of every 8 on the FMA pipe, the rest on MUFU
-                exp2_poly2(x0, x1, p0, p1);
-              } else {
-                p0 = ptx::ex2(x0);
-                p1 = ptx::ex2(x1);
-              }
-              if (e & 2)
-                l2b = fadd2(l2b, f2pack(p0, p1));
-              else
-                l2a = fadd2(l2a, f2pack(p0, p1));
-              pk[e / 2] = ptx::pack_bf16(p0, p1);
+          for (int e = 0; e < 16; e += 2) {
+            const int col = c * 16 + e;
+            // x = s * scale * log2(e) - ref  for a register pair (FFMA2)
+            const uint64_t xx = ffma2(u2pack(s[col], s[col + 1]), sc2, nref2);
+            float x0, x1, p0, p1;
+            f2unpack(xx, x0, x1);
+            if ((kPolyPairs >> ((col >> 1) & 3)) & 1) {
+              exp2_poly2(x0, x1, p0, p1);   // FMA pipe
+            } else {
+              p0 = ptx::ex2(x0);            // MUFU
+              p1 = ptx::ex2(x1);
             }
-            ptx::tmem_st16(tS + c * 16, pk);
+            if (e & 2) {
+              l2 += p0;
+              l3 += p1;
+            } else {
+              l0 += p0;
+              l1 += p1;
+            }
+            pk[e / 2] = ptx::pack_bf16(p0, p1);
           }
+          ptx::tmem_st8(tS + c * 8, pk);
         }
-        {
-          float a0, a1, b0, b1;
-          f2unpack(l2a, a0, a1);
-          f2unpack(l2b, b0, b1);
-          l_run += (a0 + a1) + (b0 + b1);
-        }
+        l_run += (l0 + l1) + (l2 + l3);
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_ready[x]);
+        TRACE_SM(21, j);
       }
       // ---------------- epilogue
       ptx::mbar_wait(&o_full[x], oph);
       oph ^= 1u;
       ptx::tc_fence_after();
+      TRACE_SM(22, 0);
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       const float lse = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
       if (f.kind == kLastQ) {
@@ -620,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
         if (valid && p.lse) p.lse[(int64_t)head * p.n + tok] = lse;
       }
+      TRACE_SM(23, 0);
       ptx::tc_fence_before();
     }
   }

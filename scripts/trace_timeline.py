@@ -1,0 +1,56 @@
+"""Debug: per-event timeline of one CTA from the TA_TRACE build (clock64 cycles)."""
+import ctypes, os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("TA_LIBRARY", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                 "paper_2507_21526_b200", "libtriattn_trace.so"))
+import torch
+import paper_2507_21526_b200 as ta
+import synth
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+dense = len(sys.argv) > 2 and sys.argv[2] == "dense"
+c = synth.CONFIGS[name]
+q, k, v = (t.cuda() for t in synth.config_qkv(c, 16))
+lib = ta._load()
+lib.ta_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+NAMES = {1: "PR.Q", 2: "PR.K", 3: "PR.V", 10: "MM.gotP_A", 11: "MM.PV_A", 12: "MM.QK_A", 13: "MM.gotP_B",
+         14: "MM.PV_B", 15: "MM.QK_B", 16: "MM.gotQ", 17: "MM.gotV", 20: "SM.gotS", 21: "SM.Pdone",
+         22: "SM.epi0", 23: "SM.epi1"}
+for cta in (0, 77):
+    os.environ["TA_TRACE_CTA"] = str(cta)
+    for _ in range(2):
+        if dense:
+            ta.dense_attn_prefill(q, k, v)
+        else:
+            ta.triangle_attn_prefill(q, k, v, sink=c.si, window=c.sl, last_q=c.last)
+    torch.cuda.synchronize()
+    buf = np.zeros(4 * 65536, dtype=np.uint64)
+    lib.ta_debug_trace_read(buf.ctypes.data, buf.nbytes)
+    ev = []
+    for role in range(4):
+        seg = buf[role * 65536:(role + 1) * 65536]
+        seg = seg[seg != 0]
+        for w in seg:
+            w = int(w)
+            code, arg, t = w >> 56, (w >> 48) & 0xff, w & 0xffffffffffff
+            ev.append((t, role, code, arg))
+    ev.sort()
+    t0 = ev[0][0]
+    print(f"=== CTA {cta}: {len(ev)} events, span {ev[-1][0]-t0} cycles")
+    for t, role, code, arg in ev[:160]:
+        lab = NAMES.get(code, str(code)) + ("" if role != 3 else "(B)") + ("(A)" if role == 2 else "")
+        print(f"{t - t0:9d} {lab:14s} {arg}")
+    # per-block statistics for softmax A/B
+    for role in (2, 3):
+        got = [t for t, r, cd, a in ev if r == role and cd == 20]
+        done = [t for t, r, cd, a in ev if r == role and cd == 21]
+        n = min(len(got), len(done))
+        d = np.array(done[:n]) - np.array(got[:n])
+        gap = np.array(got[1:n]) - np.array(done[:n - 1])
+        print(f"softmax {'AB'[role-2]}: blocks={n} compute med={np.median(d):.0f} mean={d.mean():.0f}; "
+              f"wait-for-S med={np.median(gap):.0f} mean={gap.mean():.0f}")
+    pvA = [t for t, r, cd, a in ev if r == 1 and cd == 10]
+    doneA = [t for t, r, cd, a in ev if r == 2 and cd == 21]
+    n = min(len(pvA), len(doneA))
+    print("P_A arrive -> MMA sees it: med", np.median(np.array(pvA[:n]) - np.array(doneA[:n])))
