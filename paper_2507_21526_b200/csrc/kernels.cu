@@ -76,8 +76,12 @@ constexpr int kAllocWarp = 10;
 constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
-// Bit k set: column pair k (of the 4 pairs in every 8 columns) uses the FMA-pipe exp2.
-constexpr int kPolyPairs = 0x0;            // (0: all exponentials on the MUFU)
+// Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
+// instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
+#ifndef TA_POLY_MASK
+#define TA_POLY_MASK 0x25
+#endif
+constexpr int kPolyPairs = TA_POLY_MASK;
 
 struct ItemInfo {
   int kind, kvh, pair;
@@ -277,8 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   const uint32_t it_beg = p.offsets[blockIdx.x];
   const uint32_t it_end = p.offsets[blockIdx.x + 1];
 
-  // Register split (pool = 168 x 384): producer/MMA/alloc warpgroup 88, softmax 200.
-  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+  // Register split (pool = 168 x 384): producer/MMA/alloc warpgroup 112, softmax 192.
+  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
 
   if (warp == kTmaWarp) {
     // ===================== TMA producer (whole warp, one elected lane issues) ==========
@@ -342,8 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #ifdef TA_TRACE
       uint32_t trc = 0;
 #endif
-      const uint32_t tS[2] = {tmem + 0, tmem + 128};
-      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      // TMEM columns: S_x at 128 x, O_x at 256 + 128 x
       const uint32_t qbase = ptx::smem_u32(sQ);
       const uint32_t skbase = ptx::smem_u32(sSinkK);
       const uint32_t svbase = ptx::smem_u32(sSinkV);
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           for (int s = 0; s < D / 16; ++s) {
             const uint32_t kq = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
             const uint32_t ks = ((s >> 2) * C::kSinkHalfBytes + (s & 3) * 32) >> 4;
-            ptx::mma_ss(tS[x], a0 + kq, dsk + ks, idesc_sink, s > 0 ? 1u : 0u);
+            ptx::mma_ss((tmem + 128u * x), a0 + kq, dsk + ks, idesc_sink, s > 0 ? 1u : 0u);
           }
         }
         const int nmain = b.ncols - b.sink;
@@ -377,21 +380,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #pragma unroll
           for (int s = 0; s < D / 16; ++s) {
             const uint32_t off = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
-            ptx::mma_ss(tS[x] + b.sink, a0 + off, b0 + off, idesc, s > 0 ? 1u : 0u);
+            ptx::mma_ss((tmem + 128u * x) + b.sink, a0 + off, b0 + off, idesc, s > 0 ? 1u : 0u);
           }
         }
       };
       // O_x += P_x V over the block; P_x (bf16) lives in the S_x columns.
       auto issue_pv = [&](int x, uint32_t vslot, const Blk &b, bool acc) {
         if (!leader) return;
-        if (b.sink) ptx::mma_ts(tO[x], tS[x], dsv, idesc_pv, acc ? 1u : 0u);
+        if (b.sink) ptx::mma_ts((tmem + 256u + 128u * x), (tmem + 128u * x), dsv, idesc_pv, acc ? 1u : 0u);
         const uint64_t b0 = dkv_mn + (uint64_t)((vslot * C::kSlotBytes) >> 4);
         const int ksteps = (b.ncols - b.sink) / 16;
-        const uint32_t pcol = tS[x] + b.sink / 2;
+        const uint32_t pcol = (tmem + 128u * x) + b.sink / 2;
         const uint32_t acc0 = (acc || b.sink) ? 1u : 0u;
 #pragma unroll 1
         for (int s = 0; s < ksteps; ++s)
-          ptx::mma_ts(tO[x], pcol + s * 8, b0 + (uint64_t)(s * (2048 >> 4)), idesc_pv,
+          ptx::mma_ts((tmem + 256u + 128u * x), pcol + s * 8, b0 + (uint64_t)(s * (2048 >> 4)), idesc_pv,
                       (acc0 || s > 0) ? 1u : 0u);
       };
       auto commit = [&](uint64_t *bar) {
@@ -467,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     __syncwarp();
   } else if (warp < 8) {
     // ===================== softmax / epilogue =====================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;" ::: "memory");
 
     const int x = warp / 4;         // Q tile of this warpgroup
     const int wq = warp % 4;        // TMEM lane quarter
@@ -588,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const float ref = (m_run == -INFINITY) ? 0.f : m_run;
         const uint64_t sc2 = f2pack(sc, sc);
         const uint64_t nref2 = f2pack(-ref, -ref);
-        float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+        uint64_t l2a = 0, l2b = 0;  // packed partial row sums (FADD2)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           uint32_t pk[8];
@@ -599,24 +602,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             const uint64_t xx = ffma2(u2pack(s[col], s[col + 1]), sc2, nref2);
             float x0, x1, p0, p1;
             f2unpack(xx, x0, x1);
-            if ((kPolyPairs >> ((col >> 1) & 3)) & 1) {
+            if ((kPolyPairs >> ((col >> 1) & 7)) & 1) {
               exp2_poly2(x0, x1, p0, p1);   // FMA pipe
             } else {
               p0 = ptx::ex2(x0);            // MUFU
               p1 = ptx::ex2(x1);
             }
-            if (e & 2) {
-              l2 += p0;
-              l3 += p1;
-            } else {
-              l0 += p0;
-              l1 += p1;
-            }
+            if (e & 2)
+              l2b = fadd2(l2b, f2pack(p0, p1));
+            else
+              l2a = fadd2(l2a, f2pack(p0, p1));
             pk[e / 2] = ptx::pack_bf16(p0, p1);
           }
           ptx::tmem_st8(tS + c * 8, pk);
         }
-        l_run += (l0 + l1) + (l2 + l3);
+        {
+          const uint64_t l2 = fadd2(l2a, l2b);
+          float a0, a1;
+          f2unpack(l2, a0, a1);
+          l_run += a0 + a1;
+        }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_ready[x]);
