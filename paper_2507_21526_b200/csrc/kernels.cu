@@ -57,14 +57,15 @@ struct Cfg {
   static constexpr int kHalves = D / 64;                 // 64-column (128 B) swizzle atoms
   static constexpr int kHalfBytes = kTileRows * 128;     // one 64-col region of 128 rows
   static constexpr int kQTileBytes = kTileRows * D * 2;
-  static constexpr int kSinkHalfBytes = kSinkRows * 128;  // one 64-col region of 16 rows
-  static constexpr int kSinkBytes = kSinkRows * D * 2;
-  static constexpr int kSlotBytes = kBlockKeys * D * 2;   // one K or V block
+  // A K or V slot: per 64-column half, kBlockKeys + kSinkRows rows (a fused first block
+  // puts 16 sink rows in front of up to 112 band rows; 64-row TMA boxes may overhang).
+  static constexpr int kSlotRows = kBlockKeys + kSinkRows;
+  static constexpr int kSlotHalfBytes = kSlotRows * 128;
+  static constexpr int kSlotBytes = kHalves * kSlotHalfBytes;
   static constexpr int kStages = (D == 128) ? 4 : 8;
-  static constexpr int kBoxBytes = 64 * 128;             // TMA box: 64 rows x 64 cols bf16
   static constexpr int kBarBytes = 1024;
-  static constexpr int kSmem = 1024 /*align slack*/ + 2 * kQTileBytes + 2 * kSinkBytes +
-                               kStages * kSlotBytes + kBarBytes;
+  static constexpr int kSmem = 1024 /*align slack*/ + 2 * kQTileBytes + kStages * kSlotBytes +
+                               kBarBytes;
 };
 
 constexpr int kThreads = 384;
@@ -235,9 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   uint8_t *sQ = smem;                                   // [2][kQTileBytes]
-  uint8_t *sSinkK = smem + 2 * C::kQTileBytes;           // [halves][16 rows][128 B]
-  uint8_t *sSinkV = sSinkK + C::kSinkBytes;
-  uint8_t *sKV = sSinkV + C::kSinkBytes;                 // [kStages][kSlotBytes]
+  uint8_t *sKV = smem + 2 * C::kQTileBytes;              // [kStages][kSlotBytes]
   uint64_t *bars = reinterpret_cast<uint64_t *>(sKV + C::kStages * C::kSlotBytes);
   uint64_t *kv_full = bars;
   uint64_t *kv_empty = bars + C::kStages;
@@ -298,24 +297,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       }
       uint32_t seq = 0, nitem = 0;
       const uint32_t q_bytes = 2u * C::kHalves * 128u * p.tile_tokens * p.group;
-      const uint32_t sink_bytes = 2u * C::kHalves * C::kSinkHalfBytes;
       for (uint32_t ii = it_beg; ii < it_end; ++ii, ++nitem) {
         ItemInfo f;
         item_info(p, p.items[ii], f);
         ptx::mbar_wait(q_empty, (nitem & 1u) ^ 1u);
         if (leader) {
-          ptx::mbar_arrive_expect_tx(q_full, q_bytes + (f.fused ? sink_bytes : 0u));
+          ptx::mbar_arrive_expect_tx(q_full, q_bytes);
           for (int x = 0; x < 2; ++x)
             for (int h = 0; h < C::kHalves; ++h)
               ptx::tma_load_3d(sQ + x * C::kQTileBytes + h * C::kHalfBytes, &p.tm_q, q_full, h * 64,
                                f.r0 + x * p.tile_tokens, f.kvh * p.group);
           TRACE_PR(1, nitem);
-          if (f.fused) {
-            for (int h = 0; h < C::kHalves; ++h) {
-              ptx::tma_load_3d(sSinkK + h * C::kSinkHalfBytes, &p.tm_ks, q_full, h * 64, 0, f.kvh);
-              ptx::tma_load_3d(sSinkV + h * C::kSinkHalfBytes, &p.tm_vs, q_full, h * 64, 0, f.kvh);
-            }
-          }
         }
         for (int j = 0; j < f.nb; ++j) {
           const Blk b = block_info(f, j);
@@ -325,13 +317,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             ring_pos(seq, C::kStages, slot, ph);
             ptx::mbar_wait(&kv_empty[slot], ph ^ 1u);
             if (leader) {
-              ptx::mbar_arrive_expect_tx(&kv_full[slot], nbox * C::kHalves * C::kBoxBytes);
+              ptx::mbar_arrive_expect_tx(&kv_full[slot],
+                                         (nbox * 64 + b.sink) * 128 * C::kHalves);
               const CUtensorMap *tm = kv ? &p.tm_v : &p.tm_k;
               uint8_t *dst = sKV + slot * C::kSlotBytes;
-              for (int h = 0; h < C::kHalves; ++h)
+              for (int h = 0; h < C::kHalves; ++h) {
+                if (b.sink)  // sink rows 0..15 in front of the band rows
+                  ptx::tma_load_3d(dst + h * C::kSlotHalfBytes, kv ? &p.tm_vs : &p.tm_ks,
+                                   &kv_full[slot], h * 64, 0, f.kvh);
                 for (int rb = 0; rb < nbox; ++rb)
-                  ptx::tma_load_3d(dst + h * C::kHalfBytes + rb * C::kBoxBytes, tm, &kv_full[slot],
-                                   h * 64, b.kb + rb * 64, f.kvh);
+                  ptx::tma_load_3d(dst + h * C::kSlotHalfBytes + (b.sink + rb * 64) * 128, tm,
+                                   &kv_full[slot], h * 64, b.kb + rb * 64, f.kvh);
+              }
               TRACE_PR(2 + kv, j);
             }
           }
@@ -348,54 +345,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #endif
       // TMEM columns: S_x at 128 x, O_x at 256 + 128 x
       const uint32_t qbase = ptx::smem_u32(sQ);
-      const uint32_t skbase = ptx::smem_u32(sSinkK);
-      const uint32_t svbase = ptx::smem_u32(sSinkV);
       const uint32_t kvbase = ptx::smem_u32(sKV);
       const uint32_t idesc_pv = ptx::idesc_bf16(128, D, 1);
-      const uint32_t idesc_sink = ptx::idesc_bf16(128, kSinkRows, 0);
       uint32_t seq = 0, nitem = 0;
       uint32_t pph[2] = {0, 0};
       // Descriptors are built once; per MMA only the 14-bit start-address field moves
       // (smem offsets < 256 KB, so adding (offset >> 4) to the descriptor never carries).
       const uint64_t dq = ptx::sdesc_sw128(qbase, 16, 1024);
-      const uint64_t dsk = ptx::sdesc_sw128(skbase, 16, 1024);
-      const uint64_t dsv = ptx::sdesc_sw128(svbase, C::kSinkHalfBytes, 1024);
       const uint64_t dkv = ptx::sdesc_sw128(kvbase, 16, 1024);
-      const uint64_t dkv_mn = ptx::sdesc_sw128(kvbase, C::kHalfBytes, 1024);
-      // S_x[:, cols] = Q_x K^T over the block (sink columns from the side buffer first).
+      const uint64_t dkv_mn = ptx::sdesc_sw128(kvbase, C::kSlotHalfBytes, 1024);
+      // S_x[:, 0:ncols] = Q_x K_slot^T  (K-major A and B, 8 x K=16 steps over d)
       auto issue_qk = [&](int x, uint32_t kslot, const Blk &b) {
+        if (!leader) return;
         const uint64_t a0 = dq + (uint64_t)((x * C::kQTileBytes) >> 4);
-        if (b.sink && leader) {
+        const uint64_t b0 = dkv + (uint64_t)((kslot * C::kSlotBytes) >> 4);
+        const uint32_t idesc = ptx::idesc_bf16(128, b.ncols, 0);
 #pragma unroll
-          for (int s = 0; s < D / 16; ++s) {
-            const uint32_t kq = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
-            const uint32_t ks = ((s >> 2) * C::kSinkHalfBytes + (s & 3) * 32) >> 4;
-            ptx::mma_ss((tmem + 128u * x), a0 + kq, dsk + ks, idesc_sink, s > 0 ? 1u : 0u);
-          }
-        }
-        const int nmain = b.ncols - b.sink;
-        if (nmain > 0 && leader) {
-          const uint32_t idesc = ptx::idesc_bf16(128, nmain, 0);
-          const uint64_t b0 = dkv + (uint64_t)((kslot * C::kSlotBytes) >> 4);
-#pragma unroll
-          for (int s = 0; s < D / 16; ++s) {
-            const uint32_t off = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
-            ptx::mma_ss((tmem + 128u * x) + b.sink, a0 + off, b0 + off, idesc, s > 0 ? 1u : 0u);
-          }
+        for (int s = 0; s < D / 16; ++s) {
+          const uint32_t qo = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
+          const uint32_t ko = ((s >> 2) * C::kSlotHalfBytes + (s & 3) * 32) >> 4;
+          ptx::mma_ss(tmem + 128u * x, a0 + qo, b0 + ko, idesc, s > 0 ? 1u : 0u);
         }
       };
-      // O_x += P_x V over the block; P_x (bf16) lives in the S_x columns.
+      // O_x += P_x V_slot; P_x (bf16) lives in the S_x columns; V MN-major (d contiguous).
       auto issue_pv = [&](int x, uint32_t vslot, const Blk &b, bool acc) {
         if (!leader) return;
-        if (b.sink) ptx::mma_ts((tmem + 256u + 128u * x), (tmem + 128u * x), dsv, idesc_pv, acc ? 1u : 0u);
         const uint64_t b0 = dkv_mn + (uint64_t)((vslot * C::kSlotBytes) >> 4);
-        const int ksteps = (b.ncols - b.sink) / 16;
-        const uint32_t pcol = (tmem + 128u * x) + b.sink / 2;
-        const uint32_t acc0 = (acc || b.sink) ? 1u : 0u;
-#pragma unroll 1
-        for (int s = 0; s < ksteps; ++s)
-          ptx::mma_ts((tmem + 256u + 128u * x), pcol + s * 8, b0 + (uint64_t)(s * (2048 >> 4)), idesc_pv,
-                      (acc0 || s > 0) ? 1u : 0u);
+        const int ksteps = b.ncols / 16;
+        const uint32_t pcol = tmem + 128u * x;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s < ksteps)
+            ptx::mma_ts(tmem + 256u + 128u * x, pcol + s * 8, b0 + (uint64_t)(s * (2048 >> 4)),
+                        idesc_pv, (acc || s > 0) ? 1u : 0u);
       };
       auto commit = [&](uint64_t *bar) {
         if (leader) ptx::tc_commit(bar);
@@ -418,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         issue_qk(1, kslot, b);
         commit(&s_full[1]);
         commit(&kv_empty[kslot]);
+        if (f.nb == 1) commit(q_empty);  // Q tiles are free after the item's last QK^T
         for (int j = 0; j < f.nb; ++j) {
           ring_pos(seq0 + 2 * j + 1, C::kStages, vslot, vph);
           ptx::mbar_wait(&kv_full[vslot], vph);
@@ -453,9 +436,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(14, j);
           if (!more) commit(&o_full[1]);
           commit(&kv_empty[vslot]);
-          // Q tiles and the sink K/V side buffer are free once the item's last QK^T and
-          // its block-0 PV (which reads the sink V rows) have completed.
-          if (f.nb == 1) commit(q_empty);
           if (more) {
             issue_qk(1, kslot1, b1);
             commit(&s_full[1]);
@@ -549,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #pragma unroll
         for (int c = 0; c < 8; ++c) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
         ptx::tmem_wait_ld();
+        TRACE_SM(24, j);
         if (!warp_full) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -570,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           mx3 = max3(mx3, __uint_as_float(s[e + 6]), __uint_as_float(s[e + 7]));
         }
         const float m_new = fmaxf(m_run, max3(mx0, mx1, fmaxf(mx2, mx3)) * sc);
+        TRACE_SM(25, j);
         const bool need = m_new > m_run + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
           const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
@@ -616,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           ptx::tmem_st8(tS + c * 8, pk);
         }
+        TRACE_SM(26, j);
         {
           const uint64_t l2 = fadd2(l2a, l2b);
           float a0, a1;

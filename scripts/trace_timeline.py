@@ -16,7 +16,7 @@ lib = ta._load()
 lib.ta_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 NAMES = {1: "PR.Q", 2: "PR.K", 3: "PR.V", 10: "MM.gotP_A", 11: "MM.PV_A", 12: "MM.QK_A", 13: "MM.gotP_B",
          14: "MM.PV_B", 15: "MM.QK_B", 16: "MM.gotQ", 17: "MM.gotV", 20: "SM.gotS", 21: "SM.Pdone",
-         22: "SM.epi0", 23: "SM.epi1"}
+         22: "SM.epi0", 23: "SM.epi1", 24: "SM.ldS", 25: "SM.max", 26: "SM.exp"}
 for cta in (0, 77):
     os.environ["TA_TRACE_CTA"] = str(cta)
     for _ in range(2):
@@ -50,6 +50,12 @@ for cta in (0, 77):
         gap = np.array(got[1:n]) - np.array(done[:n - 1])
         print(f"softmax {'AB'[role-2]}: blocks={n} compute med={np.median(d):.0f} mean={d.mean():.0f}; "
               f"wait-for-S med={np.median(gap):.0f} mean={gap.mean():.0f}")
+    for role in (2, 3):
+        seq = {cd: [t for t, r, c2, a in ev if r == role and c2 == cd] for cd in (20, 24, 25, 26, 21)}
+        n = min(len(v) for v in seq.values())
+        if n:
+            st = [np.median(np.array(seq[b][:n]) - np.array(seq[a][:n])) for a, b in ((20, 24), (24, 25), (25, 26), (26, 21))]
+            print(f"softmax {'AB'[role-2]} phases (median): ldS {st[0]:.0f}  max {st[1]:.0f}  exp {st[2]:.0f}  st/arrive {st[3]:.0f}")
     pvA = [t for t, r, cd, a in ev if r == 1 and cd == 10]
     doneA = [t for t, r, cd, a in ev if r == 2 and cd == 21]
     n = min(len(pvA), len(doneA))
