@@ -45,7 +45,7 @@ namespace {
   } while (0)
 #define TRACE_PR(code, arg) do { if (leader) TRACE_AT(0, trc, code, arg); } while (0)
 #define TRACE_MM(code, arg) do { if (leader) TRACE_AT(65536, trc, code, arg); } while (0)
-#define TRACE_SM(code, arg) do { if (lane == 0 && wq == 0) TRACE_AT(131072 + 65536 * x, trc, code, arg); } while (0)
+#define TRACE_SM(code, arg) do { if (lane == 0 && wq == 0 && hc == 0) TRACE_AT(131072 + 65536 * x, trc, code, arg); } while (0)
 #else
 #define TRACE_PR(code, arg) do {} while (0)
 #define TRACE_MM(code, arg) do {} while (0)
@@ -64,16 +64,19 @@ struct Cfg {
   static constexpr int kSlotBytes = kHalves * kSlotHalfBytes;
   static constexpr int kStages = (D == 128) ? 4 : 8;
   static constexpr int kBarBytes = 1024;
+  static constexpr int kRedBytes = 2 * 2 * 2 * kTileRows * 4 + 2 * 2 * kTileRows * 4;
   static constexpr int kSmem = 1024 /*align slack*/ + 2 * kQTileBytes + kStages * kSlotBytes +
-                               kBarBytes;
+                               kBarBytes + kRedBytes;
 };
 
-constexpr int kThreads = 384;
-// Warp roles.  Softmax warpgroups take the low warp ids so that the TMA producer and the
-// MMA issuer (high ids) win the highest-warp-id-first issue arbitration on their SMSPs.
-constexpr int kMmaWarp = 8;
-constexpr int kTmaWarp = 9;
-constexpr int kAllocWarp = 10;
+constexpr int kThreads = 640;
+// Warp roles.  Softmax: 8 warps per Q tile (2 threads per query row, 64 columns each);
+// warps 0-7 tile A, 8-15 tile B.  The TMA producer and the MMA issuer take the high warp
+// ids so they win the highest-warp-id-first issue arbitration on their SMSPs.
+constexpr int kSoftmaxWarps = 16;
+constexpr int kMmaWarp = 16;
+constexpr int kTmaWarp = 17;
+constexpr int kAllocWarp = 18;
 constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
@@ -195,7 +198,7 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float &y0, float 
   const uint64_t x = f2pack(x0, x1);
   const uint64_t t = fadd2(x, f2pack(kMagic, kMagic));
   const uint64_t r = fadd2(t, f2pack(-kMagic, -kMagic));
-  uint64_t f = fadd2(x, r ^ 0x8000000080000000ull);  // x - rint(x)
+  uint64_t f = ffma2(r, f2pack(-1.f, -1.f), x);    // x - rint(x), exact
   uint64_t pp = ffma2(f, f2pack(0.055008627f, 0.055008627f), f2pack(0.24221043f, 0.24221043f));
   pp = ffma2(pp, f, f2pack(0.69328302f, 0.69328302f));
   pp = ffma2(pp, f, f2pack(1.0f, 1.0f));
@@ -246,6 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   uint64_t *p_ready = q_full + 4;  // [2]
   uint64_t *o_full = q_full + 6;   // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 8);
+  // cross-warp row reductions of the two column halves of a row:
+  // red_max[tile][block parity][half][row], red_l[tile][half][row]
+  float *red_max = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bars) + C::kBarBytes);
+  float *red_l = red_max + 2 * 2 * 2 * kTileRows;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     ptx::mbar_init(q_empty, 1);
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&s_full[x], 1);
-      ptx::mbar_init(&p_ready[x], 128);
+      ptx::mbar_init(&p_ready[x], 2 * kTileRows);
       ptx::mbar_init(&o_full[x], 1);
     }
     ptx::fence_mbar_init();
@@ -280,8 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   const uint32_t it_beg = p.offsets[blockIdx.x];
   const uint32_t it_end = p.offsets[blockIdx.x + 1];
 
-  // Register split (pool = 168 x 384): producer/MMA/alloc warpgroup 112, softmax 192.
-  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
+  // Register split (pool = 96 x 640): producer/MMA/alloc warpgroup 64, softmax 104.
+  if (warp >= kSoftmaxWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;" ::: "memory");
 
   if (warp == kTmaWarp) {
     // ===================== TMA producer (whole warp, one elected lane issues) ==========
@@ -373,11 +380,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const uint64_t b0 = dkv_mn + (uint64_t)((vslot * C::kSlotBytes) >> 4);
         const int ksteps = b.ncols / 16;
         const uint32_t pcol = tmem + 128u * x;
+        // P of keys [64h, 64h + 64) sits in TMEM columns [64h, 64h + 32) of S_x (each
+        // column half written over its own S columns by its own softmax warps).
 #pragma unroll
         for (int s = 0; s < 8; ++s)
           if (s < ksteps)
-            ptx::mma_ts(tmem + 256u + 128u * x, pcol + s * 8, b0 + (uint64_t)(s * (2048 >> 4)),
-                        idesc_pv, (acc || s > 0) ? 1u : 0u);
+            ptx::mma_ts(tmem + 256u + 128u * x, pcol + (s >> 2) * 64 + (s & 3) * 8,
+                        b0 + (uint64_t)(s * (2048 >> 4)), idesc_pv, (acc || s > 0) ? 1u : 0u);
       };
       auto commit = [&](uint64_t *bar) {
         if (leader) ptx::tc_commit(bar);
@@ -448,21 +457,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       }
     }
     __syncwarp();
-  } else if (warp < 8) {
+  } else if (warp < kSoftmaxWarps) {
     // ===================== softmax / epilogue =====================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;" ::: "memory");
-
-    const int x = warp / 4;         // Q tile of this warpgroup
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;" ::: "memory");
+    const int x = warp / 8;         // Q tile of this warpgroup pair
+    const int hc = (warp / 4) & 1;  // column half: S columns [64 hc, 64 hc + 64)
     const int wq = warp % 4;        // TMEM lane quarter
     const int r = wq * 32 + lane;   // packed row = TMEM lane
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t tS = tmem + x * 128 + lane_off;
-    const uint32_t tO = tmem + 256 + x * 128 + lane_off;
+    const uint32_t tS = tmem + x * 128 + hc * 64 + lane_off;  // own S columns, own P columns
+    const uint32_t tO = tmem + 256 + x * 128 + hc * (D / 2) + lane_off;  // own O columns
     const int T = p.tile_tokens;
     const bool row_in_tile = r < p.group * T;
     const int hoff = row_in_tile ? r / T : 0;
     const int toff = row_in_tile ? r % T : 0;
     const float sc = p.scale_log2;
+    const int c0 = hc * 64;  // first S column of this thread
+    float *my_max = red_max + (x * 2 * 2 + hc) * kTileRows + r;        // + parity * 2 * 128
+    const float *peer_max = red_max + (x * 2 * 2 + (1 - hc)) * kTileRows + r;
     uint32_t sph = 0, oph = 0;
 #ifdef TA_TRACE
     uint32_t trc = 0;
@@ -474,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       const bool valid = row_in_tile && tok < p.n;
       const bool last_row = tok >= p.n - p.last;
       float m_run = -INFINITY;  // reference max, log2 units of scaled scores
-      float l_run = 0.f;        // running sum of 2^(x - m_run)
+      float l_run = 0.f;        // running sum of 2^(x - m_run) over this thread's columns
       for (int j = 0; j < f.nb; ++j) {
         const Blk b = block_info(f, j);
         // Kept columns of row i in this block: [a_lo, a_hi] U [b_lo, b_hi]   (reading R1)
@@ -506,33 +518,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           b_lo = b.kb;
           b_hi = min(tok, khi);
         }
-        // keys -> columns
+        // keys -> columns of this thread's half
         if (f.kind != kStream || !b.sink) {
           a_lo -= b.kb;
           a_hi -= b.kb;
         }
-        b_lo += b.sink - b.kb;
-        b_hi += b.sink - b.kb;
+        b_lo += b.sink - b.kb - c0;
+        b_hi += b.sink - b.kb - c0;
+        a_lo -= c0;
+        a_hi -= c0;
         norm_iv(a_lo, a_hi);
         norm_iv(b_lo, b_hi);
-        // All 128 columns are processed every block (columns >= ncols are masked): no
+        // All 64 columns are processed every block (columns >= ncols are masked): no
         // data-dependent branches inside the row loop.
-        const bool full = (b_lo <= 0 && b_hi >= 127) || (a_lo <= 0 && a_hi >= 127) ||
-                          (a_lo <= 0 && b_lo <= a_hi + 1 && b_hi >= 127);
+        const bool full = (b_lo <= 0 && b_hi >= 63) || (a_lo <= 0 && a_hi >= 63) ||
+                          (a_lo <= 0 && b_lo <= a_hi + 1 && b_hi >= 63);
         const bool warp_full = __all_sync(0xffffffffu, full);
 
         ptx::mbar_wait(&s_full[x], sph);
         sph ^= 1u;
         ptx::tc_fence_after();
         TRACE_SM(20, j);
-        uint32_t s[128];
+        uint32_t s[64];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
         ptx::tmem_wait_ld();
         TRACE_SM(24, j);
         if (!warp_full) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             // kept-column bitmask of chunk c: [a_lo, a_hi] U [b_lo, b_hi] intersected with
             // [32c, 32c + 31]
             const uint32_t m32 = iv_bits(a_lo - 32 * c, a_hi - 32 * c) | iv_bits(b_lo - 32 * c, b_hi - 32 * c);
@@ -541,16 +555,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
               s[c * 32 + e] = (m32 & (1u << e)) ? s[c * 32 + e] : 0xff800000u;  // -inf
           }
         }
-        // raw row max (scale > 0 commutes with max)
+        // raw row max over this half (scale > 0 commutes with max), then over the row
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 128; e += 8) {
+        for (int e = 0; e < 64; e += 8) {
           mx0 = max3(mx0, __uint_as_float(s[e]), __uint_as_float(s[e + 1]));
           mx1 = max3(mx1, __uint_as_float(s[e + 2]), __uint_as_float(s[e + 3]));
           mx2 = max3(mx2, __uint_as_float(s[e + 4]), __uint_as_float(s[e + 5]));
           mx3 = max3(mx3, __uint_as_float(s[e + 6]), __uint_as_float(s[e + 7]));
         }
-        const float m_new = fmaxf(m_run, max3(mx0, mx1, fmaxf(mx2, mx3)) * sc);
+        float mx = max3(mx0, mx1, fmaxf(mx2, mx3));
+        my_max[(j & 1) * 2 * kTileRows] = mx;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(8 * 32) : "memory");
+        mx = fmaxf(mx, peer_max[(j & 1) * 2 * kTileRows]);
+        const float m_new = fmaxf(m_run, mx * sc);
         TRACE_SM(25, j);
         const bool need = m_new > m_run + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
@@ -560,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           if (j > 0) {
             // O_x holds exactly blocks < j: S_x(j) completing implies PV_x(j-1) completed.
 #pragma unroll 1
-            for (int c = 0; c < D / 16; ++c) {
+            for (int c = 0; c < D / 32; ++c) {
               uint32_t o[16];
               ptx::tmem_ld16(tO + c * 16, o, 0);
               ptx::tmem_wait_ld();
@@ -575,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const uint64_t nref2 = f2pack(-ref, -ref);
         uint64_t l2a = 0, l2b = 0;  // packed partial row sums (FADD2)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 4; ++c) {
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
@@ -610,20 +628,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ptx::mbar_arrive(&p_ready[x]);
         TRACE_SM(21, j);
       }
-      // ---------------- epilogue
+      // ---------------- epilogue: each thread finalises its D/2 output columns
+      red_l[(x * 2 + hc) * kTileRows + r] = l_run;
       ptx::mbar_wait(&o_full[x], oph);
       oph ^= 1u;
       ptx::tc_fence_after();
       TRACE_SM(22, 0);
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      const float lse = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(8 * 32) : "memory");
+      const float l_row = l_run + red_l[(x * 2 + (1 - hc)) * kTileRows + r];
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(8 * 32) : "memory");  // red_l reuse
+      const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
+      const float lse = l_row > 0.f ? (m_run + __log2f(l_row)) * kLn2 : -INFINITY;
       if (f.kind == kLastQ) {
         const int64_t slot =
             ((int64_t)f.kvh * p.n_last_pairs + (f.pair - p.p_last0)) * p.s_max + f.kb0 / p.chunk_keys;
         const int64_t prow = slot * (2 * kTileRows) + x * kTileRows + r;
-        float *dst = p.part_o + prow * D;
+        float *dst = p.part_o + prow * D + hc * (D / 2);
 #pragma unroll
-        for (int c = 0; c < D / 16; ++c) {
+        for (int c = 0; c < D / 32; ++c) {
           uint32_t o[16];
           ptx::tmem_ld16(tO + c * 16, o, 0);
           ptx::tmem_wait_ld();
@@ -634,13 +656,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             *reinterpret_cast<float4 *>(dst + c * 16 + e) = v;
           }
         }
-        p.part_lse[prow] = lse;
+        if (hc == 0) p.part_lse[prow] = lse;
       } else {
         const int head = f.kvh * p.group + hoff;
         __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(p.o) +
-                             (int64_t)head * p.o_sh + (int64_t)tok * p.o_st;
+                             (int64_t)head * p.o_sh + (int64_t)tok * p.o_st + hc * (D / 2);
 #pragma unroll
-        for (int c = 0; c < D / 16; ++c) {
+        for (int c = 0; c < D / 32; ++c) {
           uint32_t o[16];
           ptx::tmem_ld16(tO + c * 16, o, 0);
           ptx::tmem_wait_ld();
@@ -654,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
           }
         }
-        if (valid && p.lse) p.lse[(int64_t)head * p.n + tok] = lse;
+        if (valid && p.lse && hc == 0) p.lse[(int64_t)head * p.n + tok] = lse;
       }
       TRACE_SM(23, 0);
       ptx::tc_fence_before();
