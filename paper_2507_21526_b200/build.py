@@ -31,10 +31,12 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
-    """Compile libtriattn.so (or, with trace=True, the debug-timeline libtriattn_trace.so)."""
-    so = SO_TRACE if trace else SO
-    if not force and not trace and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False, defines=(),
+          out: str | None = None) -> str:
+    """Compile libtriattn.so (or, with trace=True, the debug-timeline libtriattn_trace.so;
+    `defines`/`out` build tuning variants for experiments)."""
+    so = out or (SO_TRACE if trace else SO)
+    if not force and not trace and out is None and not _stale():
         return SO
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "--expt-relaxed-constexpr",
@@ -42,6 +44,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
            "-o", so + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES]
     if trace:
         cmd.insert(1, "-DTA_TRACE")
+    for d in defines:
+        cmd.insert(1, "-D" + d)
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

@@ -81,11 +81,15 @@ constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
-// instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
+// instead of MUFU.EX2; 0x11 = 1/4 of the exponentials (MUFU is 16/clk/SM on B200).
 #ifndef TA_POLY_MASK
-#define TA_POLY_MASK 0x25
+#define TA_POLY_MASK 0x11
 #endif
 constexpr int kPolyPairs = TA_POLY_MASK;
+#ifndef TA_PINGPONG
+#define TA_PINGPONG 1
+#endif
+constexpr bool kPingPong = TA_PINGPONG != 0;
 
 struct ItemInfo {
   int kind, kvh, pair;
@@ -187,6 +191,13 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   return r;
 }
 
+// (a << 23) + b with shift+add on the integer ALU pipe (keeps the FMA pipe for FFMA2).
+__device__ __forceinline__ int lea23(int a, int b) {
+  int r;
+  asm("{\n\t.reg .b32 t;\n\tshl.b32 t, %1, 23;\n\tadd.s32 %0, t, %2;\n\t}" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 // 2^x for a pair on the FMA pipe (offloads the MUFU unit): x = j + f, j = rint(x),
 // f in [-1/2, 1/2], 2^f ~ 1 + c1 f + c2 f^2 + c3 f^3 (max rel. err 1.0e-4, far below the
 // bf16 rounding of P).  x is clamped to >= -127 so that x = -inf (a masked score) gives
@@ -205,8 +216,8 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float &y0, float 
   float p0, p1, t0, t1;
   f2unpack(pp, p0, p1);
   f2unpack(t, t0, t1);
-  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
-  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+  y0 = __int_as_float(lea23(__float_as_int(t0), __float_as_int(p0)));
+  y1 = __int_as_float(lea23(__float_as_int(t1), __float_as_int(p1)));
 }
 
 __device__ __forceinline__ uint64_t u2pack(uint32_t lo, uint32_t hi) {
@@ -248,7 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   uint64_t *s_full = q_full + 2;   // [2]
   uint64_t *p_ready = q_full + 4;  // [2]
   uint64_t *o_full = q_full + 6;   // [2]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 8);
+  uint64_t *exp_turn = q_full + 8;  // [2] softmax ping-pong: tile x may run its exp phase
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 10);
   // cross-warp row reductions of the two column halves of a row:
   // red_max[tile][block parity][half][row], red_l[tile][half][row]
   float *red_max = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bars) + C::kBarBytes);
@@ -268,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       ptx::mbar_init(&s_full[x], 1);
       ptx::mbar_init(&p_ready[x], 2 * kTileRows);
       ptx::mbar_init(&o_full[x], 1);
+      ptx::mbar_init(&exp_turn[x], 8);  // one arrival per softmax warp of the other tile
     }
     ptx::fence_mbar_init();
   }
@@ -304,9 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       }
       uint32_t seq = 0, nitem = 0;
       const uint32_t q_bytes = 2u * C::kHalves * 128u * p.tile_tokens * p.group;
-      for (uint32_t ii = it_beg; ii < it_end; ++ii, ++nitem) {
-        ItemInfo f;
-        item_info(p, p.items[ii], f);
+      auto load_q = [&](const ItemInfo &f, uint32_t nitem) {
         ptx::mbar_wait(q_empty, (nitem & 1u) ^ 1u);
         if (leader) {
           ptx::mbar_arrive_expect_tx(q_full, q_bytes);
@@ -316,30 +327,47 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                                f.r0 + x * p.tile_tokens, f.kvh * p.group);
           TRACE_PR(1, nitem);
         }
-        for (int j = 0; j < f.nb; ++j) {
-          const Blk b = block_info(f, j);
-          const int nbox = ceil_div(b.nk, 64);
-          for (int kv = 0; kv < 2; ++kv, ++seq) {
-            uint32_t slot, ph;
-            ring_pos(seq, C::kStages, slot, ph);
-            ptx::mbar_wait(&kv_empty[slot], ph ^ 1u);
-            if (leader) {
-              ptx::mbar_arrive_expect_tx(&kv_full[slot],
-                                         (nbox * 64 + b.sink) * 128 * C::kHalves);
-              const CUtensorMap *tm = kv ? &p.tm_v : &p.tm_k;
-              uint8_t *dst = sKV + slot * C::kSlotBytes;
-              for (int h = 0; h < C::kHalves; ++h) {
-                if (b.sink)  // sink rows 0..15 in front of the band rows
-                  ptx::tma_load_3d(dst + h * C::kSlotHalfBytes, kv ? &p.tm_vs : &p.tm_ks,
-                                   &kv_full[slot], h * 64, 0, f.kvh);
-                for (int rb = 0; rb < nbox; ++rb)
-                  ptx::tma_load_3d(dst + h * C::kSlotHalfBytes + (b.sink + rb * 64) * 128, tm,
-                                   &kv_full[slot], h * 64, b.kb + rb * 64, f.kvh);
-              }
-              TRACE_PR(2 + kv, j);
+      };
+      auto load_kv = [&](const ItemInfo &f, int j) {
+        const Blk b = block_info(f, j);
+        const int nbox = ceil_div(b.nk, 64);
+        for (int kv = 0; kv < 2; ++kv, ++seq) {
+          uint32_t slot, ph;
+          ring_pos(seq, C::kStages, slot, ph);
+          ptx::mbar_wait(&kv_empty[slot], ph ^ 1u);
+          if (leader) {
+            ptx::mbar_arrive_expect_tx(&kv_full[slot], (nbox * 64 + b.sink) * 128 * C::kHalves);
+            const CUtensorMap *tm = kv ? &p.tm_v : &p.tm_k;
+            uint8_t *dst = sKV + slot * C::kSlotBytes;
+            for (int h = 0; h < C::kHalves; ++h) {
+              if (b.sink)  // sink rows 0..15 in front of the band rows
+                ptx::tma_load_3d(dst + h * C::kSlotHalfBytes, kv ? &p.tm_vs : &p.tm_ks,
+                                 &kv_full[slot], h * 64, 0, f.kvh);
+              for (int rb = 0; rb < nbox; ++rb)
+                ptx::tma_load_3d(dst + h * C::kSlotHalfBytes + (b.sink + rb * 64) * 128, tm,
+                                 &kv_full[slot], h * 64, b.kb + rb * 64, f.kvh);
             }
+            TRACE_PR(2 + kv, j);
           }
         }
+      };
+      // Item order on the ring: K0 V0 of item i go out as soon as their slots free up;
+      // Q(i) (which waits for the previous item's last QK^T) follows; the next item's Q
+      // tiles are prefetched into L2 one item ahead so the Q load at the item boundary is
+      // an L2 hit rather than an HBM round trip.
+      for (uint32_t ii = it_beg; ii < it_end; ++ii, ++nitem) {
+        ItemInfo f;
+        item_info(p, p.items[ii], f);
+        if (leader && ii + 1 < it_end) {
+          ItemInfo fn;
+          item_info(p, p.items[ii + 1], fn);
+          for (int x = 0; x < 2; ++x)
+            for (int h = 0; h < C::kHalves; ++h)
+              ptx::tma_prefetch_l2_3d(&p.tm_q, h * 64, fn.r0 + x * p.tile_tokens, fn.kvh * p.group);
+        }
+        load_kv(f, 0);
+        load_q(f, nitem);
+        for (int j = 1; j < f.nb; ++j) load_kv(f, j);
       }
     }
     __syncwarp();
@@ -412,6 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         if (f.nb == 1) commit(q_empty);  // Q tiles are free after the item's last QK^T
         for (int j = 0; j < f.nb; ++j) {
           ring_pos(seq0 + 2 * j + 1, C::kStages, vslot, vph);
+          TRACE_MM(9, j);
           ptx::mbar_wait(&kv_full[vslot], vph);
           TRACE_MM(17, j);
           const bool more = (j + 1 < f.nb);
@@ -422,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             ring_pos(seq0 + 2 * (j + 1), C::kStages, kslot1, kph1);
           }
           // ---- tile A: PV_A(j), then QK_A(j+1)
+          TRACE_MM(8, j);
           ptx::mbar_wait(&p_ready[0], pph[0]);
           pph[0] ^= 1u;
           ptx::tc_fence_after();
@@ -430,13 +460,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(11, j);
           if (!more) commit(&o_full[0]);
           if (more) {
+            TRACE_MM(18, j);
             ptx::mbar_wait(&kv_full[kslot1], kph1);
             ptx::tc_fence_after();
+            TRACE_MM(19, j);
             issue_qk(0, kslot1, b1);
             commit(&s_full[0]);
             TRACE_MM(12, j);
           }
           // ---- tile B: PV_B(j), then QK_B(j+1)
+          TRACE_MM(7, j);
           ptx::mbar_wait(&p_ready[1], pph[1]);
           pph[1] ^= 1u;
           ptx::tc_fence_after();
@@ -475,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     const int c0 = hc * 64;  // first S column of this thread
     float *my_max = red_max + (x * 2 * 2 + hc) * kTileRows + r;        // + parity * 2 * 128
     const float *peer_max = red_max + (x * 2 * 2 + (1 - hc)) * kTileRows + r;
-    uint32_t sph = 0, oph = 0;
+    uint32_t sph = 0, oph = 0, ecount = 0;
 #ifdef TA_TRACE
     uint32_t trc = 0;
 #endif
@@ -540,13 +573,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ptx::tc_fence_after();
         TRACE_SM(20, j);
         uint32_t s[64];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
+        // Two halves: the second TMEM load is in flight while the first half is masked.
+        ptx::tmem_ld16(tS, *reinterpret_cast<uint32_t(*)[16]>(s), 0);
+        ptx::tmem_ld16(tS + 16, *reinterpret_cast<uint32_t(*)[16]>(s + 16), 0);
         ptx::tmem_wait_ld();
+        ptx::tmem_ld16(tS + 32, *reinterpret_cast<uint32_t(*)[16]>(s + 32), 0);
+        ptx::tmem_ld16(tS + 48, *reinterpret_cast<uint32_t(*)[16]>(s + 48), 0);
         TRACE_SM(24, j);
-        if (!warp_full) {
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < 2; ++c) {
+          if (c == 1) ptx::tmem_wait_ld();
+          if (!warp_full) {
             // kept-column bitmask of chunk c: [a_lo, a_hi] U [b_lo, b_hi] intersected with
             // [32c, 32c + 31]
             const uint32_t m32 = iv_bits(a_lo - 32 * c, a_hi - 32 * c) | iv_bits(b_lo - 32 * c, b_hi - 32 * c);
@@ -589,6 +626,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
         }
         const float ref = (m_run == -INFINITY) ? 0.f : m_run;
+        // Ping-pong with the other tile: the exp phases (MUFU-heavy) of the two Q tiles
+        // alternate, so each runs at full SMSP throughput while the tensor core works on
+        // the other tile.
+        if (kPingPong) ptx::mbar_wait(&exp_turn[x], (ecount & 1u) ^ (x == 0 ? 1u : 0u));
         const uint64_t sc2 = f2pack(sc, sc);
         const uint64_t nref2 = f2pack(-ref, -ref);
         uint64_t l2a = 0, l2b = 0;  // packed partial row sums (FADD2)
@@ -616,6 +657,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           ptx::tmem_st8(tS + c * 8, pk);
         }
+        __syncwarp();
+        if (kPingPong && lane == 0) ptx::mbar_arrive(&exp_turn[1 - x]);
+        ++ecount;
         TRACE_SM(26, j);
         {
           const uint64_t l2 = fadd2(l2a, l2b);

@@ -14,7 +14,7 @@ c = synth.CONFIGS[name]
 q, k, v = (t.cuda() for t in synth.config_qkv(c, 16))
 lib = ta._load()
 lib.ta_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-NAMES = {1: "PR.Q", 2: "PR.K", 3: "PR.V", 10: "MM.gotP_A", 11: "MM.PV_A", 12: "MM.QK_A", 13: "MM.gotP_B",
+NAMES = {7: "MM.waitP_B", 8: "MM.waitP_A", 9: "MM.waitV", 18: "MM.waitK", 19: "MM.gotK", 1: "PR.Q", 2: "PR.K", 3: "PR.V", 10: "MM.gotP_A", 11: "MM.PV_A", 12: "MM.QK_A", 13: "MM.gotP_B",
          14: "MM.PV_B", 15: "MM.QK_B", 16: "MM.gotQ", 17: "MM.gotV", 20: "SM.gotS", 21: "SM.Pdone",
          22: "SM.epi0", 23: "SM.epi1", 24: "SM.ldS", 25: "SM.max", 26: "SM.exp"}
 for cta in (0, 77):
@@ -56,6 +56,20 @@ for cta in (0, 77):
         if n:
             st = [np.median(np.array(seq[b][:n]) - np.array(seq[a][:n])) for a, b in ((20, 24), (24, 25), (25, 26), (26, 21))]
             print(f"softmax {'AB'[role-2]} phases (median): ldS {st[0]:.0f}  max {st[1]:.0f}  exp {st[2]:.0f}  st/arrive {st[3]:.0f}")
+    # MMA warp idle time by what it waits for (pairs of wait-start / wait-end events)
+    mm = [(t, cd) for t, r, cd, a in ev if r == 1]
+    waits = {"V": 0, "K": 0, "P_A": 0, "P_B": 0}
+    pairs = {9: (17, "V"), 18: (19, "K"), 8: (10, "P_A"), 7: (13, "P_B")}
+    for i in range(len(mm) - 1):
+        t, cd = mm[i]
+        if cd in pairs:
+            end_cd, nm = pairs[cd]
+            for t2, cd2 in mm[i + 1:i + 4]:
+                if cd2 == end_cd:
+                    waits[nm] += t2 - t
+                    break
+    span = mm[-1][0] - mm[0][0]
+    print("MMA warp wait fractions:", {k: round(v / span, 3) for k, v in waits.items()}, "span", span)
     pvA = [t for t, r, cd, a in ev if r == 1 and cd == 10]
     doneA = [t for t, r, cd, a in ev if r == 2 and cd == 21]
     n = min(len(pvA), len(doneA))
