@@ -216,6 +216,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
+    from paper_2507_21526_b200 import shard
     c = synth.CONFIGS[args.workload]
     if c.hkv % world != 0:
         raise SystemExit(f"kv heads {c.hkv} not divisible by world size {world}")
@@ -223,9 +224,7 @@ def main():
     g = c.hq // c.hkv
     hq_l = hkv_l * g
     q, k, v = synth.config_qkv(c, layer=16)      # CPU bf16, same recipe as the parity tests
-    qs = q[rank * hq_l:(rank + 1) * hq_l].contiguous()
-    ks = k[rank * hkv_l:(rank + 1) * hkv_l].contiguous()
-    vs = v[rank * hkv_l:(rank + 1) * hkv_l].contiguous()
+    qs, ks, vs = (t.contiguous() for t in shard.shard_qkv(q, k, v, rank, world))
     qd, kd, vd = qs.to(dev), ks.to(dev), vs.to(dev)
     od = torch.empty_like(qd)
     o_full = torch.empty((c.hq, c.n, c.d), dtype=torch.bfloat16, device=dev) if world > 1 else None
@@ -238,7 +237,7 @@ def main():
         else:
             ta.triangle_attn_prefill(qd, kd, vd, od, sink=c.si, window=c.sl, last_q=c.last)
         if world > 1:
-            dist.all_gather_into_tensor(o_full, od)
+            shard.gather_heads(od, world, out=o_full)
 
     def barrier():
         torch.cuda.synchronize()
