@@ -13,10 +13,12 @@ namespace ta {
 // must live in param space so cp.async.bulk.tensor can take their address.
 struct alignas(64) AttnParams {
   CUtensorMap tm_q;  // Q [Hq][N][d]:   dims {d, N, Hq},  box {64, T, G}
-  CUtensorMap tm_k;  // K [Hkv][N][d]:  dims {d, N, Hkv}, box {64, 64, 1}
+  CUtensorMap tm_k;  // K [Hkv][N][d]:  dims {d, N, Hkv}, box {64, 128, 1}
   CUtensorMap tm_v;  // V, same as K
   CUtensorMap tm_ks; // K sink rows: box {64, 16, 1}
   CUtensorMap tm_vs; // V sink rows
+  CUtensorMap tm_kb; // K band rows of a fused first block: box {64, 112, 1}
+  CUtensorMap tm_vb; // V, same
   void *o;           // bf16 O [Hq][N][d] with element strides below
   int64_t o_sh, o_st;
   float *lse;        // optional [Hq][N]

@@ -57,16 +57,17 @@ struct Cfg {
   static constexpr int kHalves = D / 64;                 // 64-column (128 B) swizzle atoms
   static constexpr int kHalfBytes = kTileRows * 128;     // one 64-col region of 128 rows
   static constexpr int kQTileBytes = kTileRows * D * 2;
-  // A K or V slot: per 64-column half, kBlockKeys + kSinkRows rows (a fused first block
-  // puts 16 sink rows in front of up to 112 band rows; 64-row TMA boxes may overhang).
-  static constexpr int kSlotRows = kBlockKeys + kSinkRows;
+  // A K or V slot: per 64-column half, 128 key rows (a fused first block puts 16 sink rows
+  // in front of 112 band rows).
+  static constexpr int kSlotRows = kBlockKeys;
   static constexpr int kSlotHalfBytes = kSlotRows * 128;
   static constexpr int kSlotBytes = kHalves * kSlotHalfBytes;
   static constexpr int kStages = (D == 128) ? 4 : 8;
   static constexpr int kBarBytes = 1024;
-  static constexpr int kRedBytes = 2 * 2 * 2 * kTileRows * 4 + 2 * 2 * kTileRows * 4;
+  static constexpr int kRedBytes = 2 * 2 * 2 * kTileRows * 4 + 2 * 2 * 2 * kTileRows * 4;
+  static constexpr int kStageBytes = 16 * 1024;  // epilogue transpose: 1 KB per softmax warp
   static constexpr int kSmem = 1024 /*align slack*/ + 2 * kQTileBytes + kStages * kSlotBytes +
-                               kBarBytes + kRedBytes;
+                               kBarBytes + kRedBytes + kStageBytes;
 };
 
 constexpr int kThreads = 640;
@@ -235,6 +236,13 @@ __device__ __forceinline__ uint32_t iv_bits(int lo, int hi) {
   return upto_hi & ~((1u << lo) - 1u);
 }
 
+// 256-bit global store (STG.E.256 on sm_100a); p must be 32-byte aligned.
+__device__ __forceinline__ void st_global_v8(void *p, const uint32_t *v) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 // Normalise a column interval; empty -> [kEmpty, kEmpty].
 __device__ __forceinline__ void norm_iv(int &lo, int &hi) {
   if (lo > hi) {
@@ -265,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   // red_max[tile][block parity][half][row], red_l[tile][half][row]
   float *red_max = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bars) + C::kBarBytes);
   float *red_l = red_max + 2 * 2 * 2 * kTileRows;
+  uint8_t *stage = reinterpret_cast<uint8_t *>(red_l + 2 * 2 * 2 * kTileRows);  // [16 warps][1 KB]
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -330,22 +339,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       };
       auto load_kv = [&](const ItemInfo &f, int j) {
         const Blk b = block_info(f, j);
-        const int nbox = ceil_div(b.nk, 64);
         for (int kv = 0; kv < 2; ++kv, ++seq) {
           uint32_t slot, ph;
           ring_pos(seq, C::kStages, slot, ph);
           ptx::mbar_wait(&kv_empty[slot], ph ^ 1u);
           if (leader) {
-            ptx::mbar_arrive_expect_tx(&kv_full[slot], (nbox * 64 + b.sink) * 128 * C::kHalves);
-            const CUtensorMap *tm = kv ? &p.tm_v : &p.tm_k;
+            // one 128-row box, or 16 sink rows + a 112-row band box (fused first block)
+            ptx::mbar_arrive_expect_tx(&kv_full[slot], kBlockKeys * 128 * C::kHalves);
             uint8_t *dst = sKV + slot * C::kSlotBytes;
             for (int h = 0; h < C::kHalves; ++h) {
-              if (b.sink)  // sink rows 0..15 in front of the band rows
+              if (b.sink) {
                 ptx::tma_load_3d(dst + h * C::kSlotHalfBytes, kv ? &p.tm_vs : &p.tm_ks,
                                  &kv_full[slot], h * 64, 0, f.kvh);
-              for (int rb = 0; rb < nbox; ++rb)
-                ptx::tma_load_3d(dst + h * C::kSlotHalfBytes + (b.sink + rb * 64) * 128, tm,
-                                 &kv_full[slot], h * 64, b.kb + rb * 64, f.kvh);
+                ptx::tma_load_3d(dst + h * C::kSlotHalfBytes + kSinkRows * 128,
+                                 kv ? &p.tm_vb : &p.tm_kb, &kv_full[slot], h * 64, b.kb, f.kvh);
+              } else {
+                ptx::tma_load_3d(dst + h * C::kSlotHalfBytes, kv ? &p.tm_v : &p.tm_k,
+                                 &kv_full[slot], h * 64, b.kb, f.kvh);
+              }
             }
             TRACE_PR(2 + kv, j);
           }
@@ -419,17 +430,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       auto commit = [&](uint64_t *bar) {
         if (leader) ptx::tc_commit(bar);
       };
-      for (uint32_t ii = it_beg; ii < it_end; ++ii, ++nitem) {
+      // The MMA stream is flat across items: [PV_A(j), QK_A(j+1), PV_B(j), QK_B(j+1)] where
+      // block j+1 may be block 0 of the next item, so a new item's first QK^T overlaps the
+      // previous item's last softmax instead of draining the pipeline.
+      if (it_beg < it_end) {
         ItemInfo f;
-        item_info(p, p.items[ii], f);
+        item_info(p, p.items[it_beg], f);
+        uint32_t ii = it_beg;
+        int j = 0;
         ptx::mbar_wait(q_full, nitem & 1u);
         ptx::tc_fence_after();
         TRACE_MM(16, nitem);
-        const uint32_t seq0 = seq;
-        seq += 2u * f.nb;
-        uint32_t kslot, kph, vslot, vph;
         Blk b = block_info(f, 0);
-        ring_pos(seq0, C::kStages, kslot, kph);
+        uint32_t kslot, kph, vslot, vph;
+        ring_pos(seq, C::kStages, kslot, kph);
         ptx::mbar_wait(&kv_full[kslot], kph);
         ptx::tc_fence_after();
         issue_qk(0, kslot, b);
@@ -438,19 +452,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         commit(&s_full[1]);
         commit(&kv_empty[kslot]);
         if (f.nb == 1) commit(q_empty);  // Q tiles are free after the item's last QK^T
-        for (int j = 0; j < f.nb; ++j) {
-          ring_pos(seq0 + 2 * j + 1, C::kStages, vslot, vph);
+        while (true) {
+          ring_pos(seq + 1, C::kStages, vslot, vph);
           TRACE_MM(9, j);
           ptx::mbar_wait(&kv_full[vslot], vph);
           TRACE_MM(17, j);
-          const bool more = (j + 1 < f.nb);
+          // next block in the flat stream (same item j+1, or block 0 of the next item)
+          const bool last = (j + 1 == f.nb);
+          const bool more = !last || (ii + 1 < it_end);
+          ItemInfo f1 = f;
+          int j1 = j + 1;
+          if (last && more) {
+            item_info(p, p.items[ii + 1], f1);
+            j1 = 0;
+          }
           Blk b1 = b;
           uint32_t kslot1 = 0, kph1 = 0;
           if (more) {
-            b1 = block_info(f, j + 1);
-            ring_pos(seq0 + 2 * (j + 1), C::kStages, kslot1, kph1);
+            b1 = block_info(f1, j1);
+            ring_pos(seq + 2, C::kStages, kslot1, kph1);
           }
-          // ---- tile A: PV_A(j), then QK_A(j+1)
+          // ---- tile A: PV_A(j), then QK_A(next)
           TRACE_MM(8, j);
           ptx::mbar_wait(&p_ready[0], pph[0]);
           pph[0] ^= 1u;
@@ -458,8 +480,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(10, j);
           issue_pv(0, vslot, b, j > 0);
           TRACE_MM(11, j);
-          if (!more) commit(&o_full[0]);
+          if (last) commit(&o_full[0]);
           if (more) {
+            if (last) {  // the next item's Q tiles
+              ++nitem;
+              ptx::mbar_wait(q_full, nitem & 1u);
+              TRACE_MM(16, nitem);
+            }
             TRACE_MM(18, j);
             ptx::mbar_wait(&kv_full[kslot1], kph1);
             ptx::tc_fence_after();
@@ -468,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             commit(&s_full[0]);
             TRACE_MM(12, j);
           }
-          // ---- tile B: PV_B(j), then QK_B(j+1)
+          // ---- tile B: PV_B(j), then QK_B(next)
           TRACE_MM(7, j);
           ptx::mbar_wait(&p_ready[1], pph[1]);
           pph[1] ^= 1u;
@@ -476,15 +503,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(13, j);
           issue_pv(1, vslot, b, j > 0);
           TRACE_MM(14, j);
-          if (!more) commit(&o_full[1]);
+          if (last) commit(&o_full[1]);
           commit(&kv_empty[vslot]);
-          if (more) {
-            issue_qk(1, kslot1, b1);
-            commit(&s_full[1]);
-            TRACE_MM(15, j);
-            commit(&kv_empty[kslot1]);
-            if (j + 2 == f.nb) commit(q_empty);
-          }
+          seq += 2;
+          if (!more) break;
+          issue_qk(1, kslot1, b1);
+          commit(&s_full[1]);
+          TRACE_MM(15, j);
+          commit(&kv_empty[kslot1]);
+          if (j1 + 1 == f1.nb) commit(q_empty);  // last QK^T of that item issued
+          if (last) ++ii;
+          f = f1;
+          j = j1;
           b = b1;
         }
       }
@@ -673,14 +703,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         TRACE_SM(21, j);
       }
       // ---------------- epilogue: each thread finalises its D/2 output columns
-      red_l[(x * 2 + hc) * kTileRows + r] = l_run;
+      // row sum of the two half-row threads (double-buffered by item parity: one barrier)
+      float *lbuf = red_l + (oph & 1u) * 2 * 2 * kTileRows;
+      lbuf[(x * 2 + hc) * kTileRows + r] = l_run;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(8 * 32) : "memory");
+      const float l_row = l_run + lbuf[(x * 2 + (1 - hc)) * kTileRows + r];
       ptx::mbar_wait(&o_full[x], oph);
       oph ^= 1u;
       ptx::tc_fence_after();
       TRACE_SM(22, 0);
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(8 * 32) : "memory");
-      const float l_row = l_run + red_l[(x * 2 + (1 - hc)) * kTileRows + r];
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(8 * 32) : "memory");  // red_l reuse
+      uint32_t ov[D / 2];
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) ptx::tmem_ld16(tO + c * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + c * 16), 0);
+      ptx::tmem_wait_ld();
+      TRACE_SM(27, 0);
       const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
       const float lse = l_row > 0.f ? (m_run + __log2f(l_row)) * kLn2 : -INFINITY;
       if (f.kind == kLastQ) {
@@ -688,37 +724,52 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             ((int64_t)f.kvh * p.n_last_pairs + (f.pair - p.p_last0)) * p.s_max + f.kb0 / p.chunk_keys;
         const int64_t prow = slot * (2 * kTileRows) + x * kTileRows + r;
         float *dst = p.part_o + prow * D + hc * (D / 2);
+        uint32_t fv[D / 2];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[16];
-          ptx::tmem_ld16(tO + c * 16, o, 0);
-          ptx::tmem_wait_ld();
+        for (int e = 0; e < D / 2; ++e) fv[e] = __float_as_uint(__uint_as_float(ov[e]) * inv);
 #pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            float4 v = make_float4(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv,
-                                   __uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-            *reinterpret_cast<float4 *>(dst + c * 16 + e) = v;
-          }
-        }
+        for (int e = 0; e < D / 2; e += 8) st_global_v8(dst + e, fv + e);  // 32 B per lane
         if (hc == 0) p.part_lse[prow] = lse;
       } else {
         const int head = f.kvh * p.group + hoff;
         __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(p.o) +
                              (int64_t)head * p.o_sh + (int64_t)tok * p.o_st + hc * (D / 2);
+        uint32_t pk[D / 4];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[16];
-          ptx::tmem_ld16(tO + c * 16, o, 0);
-          ptx::tmem_wait_ld();
-          uint32_t pk[8];
+        for (int e = 0; e < D / 4; ++e)
+          pk[e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+        // Coalesced store through a 1 KB per-warp transpose: 8 rows per round are staged
+        // (XOR-swizzled 16-byte pieces), then each STG.128 covers whole row halves
+        // (4 rows x 128 B for d = 128) instead of 32 rows x 16 B.
+        constexpr int NP = D / 16;        // 16-byte pieces per thread (row half)
+        constexpr int RPR = 32 / NP;      // rows covered by one warp-wide read
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        const uint64_t my_addr = reinterpret_cast<uint64_t>(dst);
+        uint8_t *stg = stage + warp * 1024;
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            pk[e] = ptx::pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
-          if (valid) {
-            uint4 *d4 = reinterpret_cast<uint4 *>(dst + c * 16);
-            d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        for (int q = 0; q < 4; ++q) {
+          if ((lane >> 3) == q) {
+            const int rr = lane & 7;
+#pragma unroll
+            for (int pc = 0; pc < NP; ++pc)
+              *reinterpret_cast<uint4 *>(stg + rr * NP * 16 + ((pc ^ (rr % NP)) << 4)) =
+                  make_uint4(pk[4 * pc], pk[4 * pc + 1], pk[4 * pc + 2], pk[4 * pc + 3]);
           }
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < 8 / RPR; ++h) {
+            const int rr = h * RPR + lane / NP, pc = lane % NP;
+            const uint4 v4 =
+                *reinterpret_cast<const uint4 *>(stg + rr * NP * 16 + ((pc ^ (rr % NP)) << 4));
+            const int row = q * 8 + rr;  // warp-local row whose piece this lane stores
+            const uint64_t a = __shfl_sync(0xffffffffu, my_addr, row);
+#ifndef TA_EXP_NOSTORE
+            if ((vmask >> row) & 1u) *reinterpret_cast<uint4 *>(a + (pc << 4)) = v4;
+#else
+            if (v4.x == 0x7fffffffu && ((vmask >> row) & 1u)) *reinterpret_cast<uint4 *>(a + (pc << 4)) = v4;
+#endif
+          }
+          __syncwarp();
         }
         if (valid && p.lse && hc == 0) p.lse[(int64_t)head * p.n + tok] = lse;
       }

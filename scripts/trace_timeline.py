@@ -16,7 +16,7 @@ lib = ta._load()
 lib.ta_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 NAMES = {7: "MM.waitP_B", 8: "MM.waitP_A", 9: "MM.waitV", 18: "MM.waitK", 19: "MM.gotK", 1: "PR.Q", 2: "PR.K", 3: "PR.V", 10: "MM.gotP_A", 11: "MM.PV_A", 12: "MM.QK_A", 13: "MM.gotP_B",
          14: "MM.PV_B", 15: "MM.QK_B", 16: "MM.gotQ", 17: "MM.gotV", 20: "SM.gotS", 21: "SM.Pdone",
-         22: "SM.epi0", 23: "SM.epi1", 24: "SM.ldS", 25: "SM.max", 26: "SM.exp"}
+         22: "SM.epi0", 23: "SM.epi1", 24: "SM.ldS", 25: "SM.max", 26: "SM.exp", 27: "SM.epiO"}
 for cta in (0, 77):
     os.environ["TA_TRACE_CTA"] = str(cta)
     for _ in range(2):
@@ -70,6 +70,21 @@ for cta in (0, 77):
                     break
     span = mm[-1][0] - mm[0][0]
     print("MMA warp wait fractions:", {k: round(v / span, 3) for k, v in waits.items()}, "span", span)
+    # per item: MM.gotQ to next MM.gotQ, blocks = number of MM.gotV in between
+    gq = [i for i, e in enumerate(ev) if e[1] == 1 and e[2] == 16]
+    per = {}
+    for a, b in zip(gq, gq[1:]):
+        nb = sum(1 for e in ev[a:b] if e[1] == 1 and e[2] == 17)
+        per.setdefault(nb, []).append(ev[b][0] - ev[a][0])
+    if len(gq) > 6:
+        a, b = gq[4], gq[6]
+        print("--- events of two consecutive items (from MM.gotQ #4):")
+        for t_, r_, cd_, a_ in ev[a - 20:b + 5]:
+            lab = NAMES.get(cd_, str(cd_)) + ("(B)" if r_ == 3 else "(A)" if r_ == 2 else "")
+            print(f"{t_ - ev[a][0]:9d} {lab:14s} {a_}")
+    for nb in sorted(per):
+        v = np.array(per[nb])
+        print(f"items with {nb:4d} blocks: n={len(v):4d} median {np.median(v):8.0f} cycles = {np.median(v)/max(nb,1):7.0f}/block")
     pvA = [t for t, r, cd, a in ev if r == 1 and cd == 10]
     doneA = [t for t, r, cd, a in ev if r == 2 and cd == 21]
     n = min(len(pvA), len(doneA))
