@@ -4,6 +4,7 @@
 // Compile with -gencode arch=compute_100a,code=sm_100a.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace ta {
 namespace ptx {
@@ -41,8 +42,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
 }
 // Blocks until the phase with the given parity has completed.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef TA_WATCHDOG
+  // debug builds: report and trap on a wait that never completes (pipeline deadlock)
+  uint64_t spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++spins == (1ull << 22)) {
+      printf("[watchdog] block %d thread %d stuck on mbarrier smem+%u parity %u\n", blockIdx.x,
+             threadIdx.x, smem_u32(bar) & 0xffff, parity);
+      asm volatile("trap;");
+    }
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // One lane of a converged warp (the same lane every call) returns true.
