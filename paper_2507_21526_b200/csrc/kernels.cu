@@ -46,10 +46,12 @@ namespace {
 #define TRACE_PR(code, arg) do { if (leader) TRACE_AT(0, trc, code, arg); } while (0)
 #define TRACE_MM(code, arg) do { if (leader) TRACE_AT(65536, trc, code, arg); } while (0)
 #define TRACE_SM(code, arg) do { if (lane == 0 && wq == 0 && hc == 0) TRACE_AT(131072 + 65536 * x, trc, code, arg); } while (0)
+#define TRACE_EP(code, arg) do { if (lane == 0 && eq == 0 && x0 == 0) TRACE_AT(262144, trc, code, arg); } while (0)
 #else
 #define TRACE_PR(code, arg) do {} while (0)
 #define TRACE_MM(code, arg) do {} while (0)
 #define TRACE_SM(code, arg) do {} while (0)
+#define TRACE_EP(code, arg) do {} while (0)
 #endif
 
 template <int D>
@@ -65,7 +67,7 @@ struct Cfg {
   static constexpr int kStages = (D == 128) ? 4 : 8;
   static constexpr int kBarBytes = 1024;
   static constexpr int kRedBytes = 2 * 2 * 2 * kTileRows * 4 * 2 + 2 * 2 * kTileRows * 4;
-  static constexpr int kStageBytes = 4 * 1024;  // epilogue transpose: 1 KB per epilogue warp
+  static constexpr int kStageBytes = 8 * 1024;  // epilogue transpose: 1 KB per epilogue warp (<= 8)
   static constexpr int kSmem = 1024 /*align slack*/ + 2 * kQTileBytes + kStages * kSlotBytes +
                                kBarBytes + kRedBytes + kStageBytes;
 };
@@ -80,15 +82,20 @@ struct Cfg {
 #endif
 constexpr int kHPR = TA_HPR;
 constexpr int kSoftmaxWarps = 8 * kHPR;
-constexpr int kEpiWarp0 = kSoftmaxWarps;
-constexpr int kMmaWarp = kEpiWarp0 + 4;
-constexpr int kTmaWarp = kEpiWarp0 + 5;
-constexpr int kAllocWarp = kEpiWarp0 + 6;
-constexpr int kThreads = 32 * (kSoftmaxWarps + 8);
+constexpr int kEpiWarp0 = kSoftmaxWarps;  // epilogue warps: 4 per Q tile (TA_EPI_WARPS = 8) or
+#ifndef TA_EPI_WARPS                       // 4 serving both tiles in turn (default)
+#define TA_EPI_WARPS 4
+#endif
+constexpr int kEpiWarps = TA_EPI_WARPS;
+constexpr int kMmaWarp = kEpiWarp0 + kEpiWarps;
+constexpr int kTmaWarp = kMmaWarp + 1;
+constexpr int kAllocWarp = kMmaWarp + 2;
+constexpr int kThreads = 32 * (kSoftmaxWarps + kEpiWarps + 4);
 constexpr int kNCol = 128 / kHPR;  // S columns per softmax thread
 // setmaxnreg split of the register file (launch: 65536 / kThreads, rounded down to 8)
-constexpr int kRegSoftmax = kHPR == 1 ? 184 : 96;
-constexpr int kRegOther = kHPR == 1 ? 72 : 48;
+constexpr int kRegSoftmax = kEpiWarps == 4 ? (kHPR == 1 ? 184 : 96) : (kHPR == 1 ? 176 : 88);
+constexpr int kRegEpi = kEpiWarps == 4 ? (kHPR == 1 ? 72 : 48) : 40;
+constexpr int kRegOther = kEpiWarps == 4 ? kRegEpi : (kHPR == 1 ? 48 : 40);
 constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
@@ -357,8 +364,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   const uint32_t it_beg = p.offsets[blockIdx.x];
   const uint32_t it_end = p.offsets[blockIdx.x + 1];
 
-  // Register split: softmax warpgroups kRegSoftmax, epilogue / issuer warpgroups kRegOther.
-  if (warp >= kSoftmaxWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegOther) : "memory");
+  // Register split: softmax warpgroups kRegSoftmax, epilogue kRegEpi, issuers kRegOther.
+  if (warp >= kMmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegOther) : "memory");
+  else if (warp >= kEpiWarp0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegEpi) : "memory");
 
   if (warp == kTmaWarp) {
     // ===================== TMA producer (whole warp, one elected lane issues) ==========
@@ -772,30 +780,36 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ++kitem_sm;
       }
     }
-  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     // ===================== epilogue warpgroup =====================
     // O_x = O_x / l per row from TMEM -> bf16 global (STREAM / DENSE) or fp32 split-K
     // partial + LSE (LASTQ); then O_x's TMEM columns are released to the MMA issuer.
     const int eq = warp % 4;           // TMEM lane quarter
+    const int x0 = kEpiWarps == 8 ? (warp - kEpiWarp0) / 4 : 0;  // first Q tile served
     const int r = eq * 32 + lane;      // packed row
     const uint32_t lane_off = (uint32_t)(eq * 32) << 16;
     const int T = p.tile_tokens;
     const bool row_in_tile = r < p.group * T;
     const int hoff = row_in_tile ? r / T : 0;
     const int toff = row_in_tile ? r % T : 0;
-    const uint32_t stg_s = ptx::smem_u32(stage + eq * 1024);
+    const uint32_t stg_s = ptx::smem_u32(stage + (warp - kEpiWarp0) * 1024);
     uint32_t kitem = 0;
+#ifdef TA_TRACE
+    uint32_t trc = 0;
+#endif
     for (uint32_t ii = it_beg; ii < it_end; ++ii, ++kitem) {
       ItemInfo f;
       item_info(p, p.items[ii], f);
       const uint32_t par = kitem & 1u;
-      for (int x = 0; x < 2; ++x) {
+      for (int x = x0; x < (kEpiWarps == 8 ? x0 + 1 : 2); ++x) {
         const uint32_t tO = tmem + 256 + x * 128 + lane_off;
         const int tok = f.r0 + x * T + toff;
         const bool valid = row_in_tile && tok < p.n;
+        TRACE_EP(30 + x, kitem);
         ptx::mbar_wait(&l_ready[x], par);
         ptx::mbar_wait(&o_full[x], par);
         ptx::tc_fence_after();
+        TRACE_EP(32 + x, kitem);
         const float l_row = lds_f32(ptx::smem_u32(red_l + ((par * 2 + x) * 2 + 0) * kTileRows + r)) +
                             lds_f32(ptx::smem_u32(red_l + ((par * 2 + x) * 2 + 1) * kTileRows + r));
         const float m_row = lds_f32(ptx::smem_u32(red_m + (par * 2 + x) * kTileRows + r));
@@ -838,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 pk[c * 8 + e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv,
                                                __uint_as_float(ov[2 * e + 1]) * inv);
             }
-#ifdef TA_EPI_DIRECT
+#ifndef TA_EPI_TRANSPOSE
             if (valid)
 #pragma unroll
               for (int pc = 0; pc < 8; ++pc)
@@ -869,6 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           if (valid && p.lse) p.lse[(int64_t)head * p.n + tok] = lse;
         }
         // O_x has been read: the next item's first PV_x may overwrite it
+        TRACE_EP(34 + x, kitem);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&o_free[x]);

@@ -16,7 +16,7 @@ lib = ta._load()
 lib.ta_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 NAMES = {7: "MM.waitP_B", 8: "MM.waitP_A", 9: "MM.waitV", 18: "MM.waitK", 19: "MM.gotK", 1: "PR.Q", 2: "PR.K", 3: "PR.V", 10: "MM.gotP_A", 11: "MM.PV_A", 12: "MM.QK_A", 13: "MM.gotP_B",
          14: "MM.PV_B", 15: "MM.QK_B", 16: "MM.gotQ", 17: "MM.gotV", 20: "SM.gotS", 21: "SM.Pdone",
-         22: "SM.epi0", 23: "SM.epi1", 24: "SM.ldS", 25: "SM.max", 26: "SM.exp", 27: "SM.epiO"}
+         22: "SM.epi0", 23: "SM.epi1", 24: "SM.ldS", 25: "SM.max", 26: "SM.exp", 27: "SM.epiO", 30: "EP.waitA", 31: "EP.waitB", 32: "EP.gotA", 33: "EP.gotB", 34: "EP.doneA", 35: "EP.doneB"}
 for cta in (0, 77):
     os.environ["TA_TRACE_CTA"] = str(cta)
     for _ in range(2):
@@ -25,10 +25,10 @@ for cta in (0, 77):
         else:
             ta.triangle_attn_prefill(q, k, v, sink=c.si, window=c.sl, last_q=c.last)
     torch.cuda.synchronize()
-    buf = np.zeros(4 * 65536, dtype=np.uint64)
+    buf = np.zeros(5 * 65536, dtype=np.uint64)
     lib.ta_debug_trace_read(buf.ctypes.data, buf.nbytes)
     ev = []
-    for role in range(4):
+    for role in range(5):
         seg = buf[role * 65536:(role + 1) * 65536]
         seg = seg[seg != 0]
         for w in seg:
@@ -85,6 +85,12 @@ for cta in (0, 77):
     for nb in sorted(per):
         v = np.array(per[nb])
         print(f"items with {nb:4d} blocks: n={len(v):4d} median {np.median(v):8.0f} cycles = {np.median(v)/max(nb,1):7.0f}/block")
+    ga = [t for t, r, cd, a in ev if r == 4 and cd == 32]; da = [t for t, r, cd, a in ev if r == 4 and cd == 34]
+    gb = [t for t, r, cd, a in ev if r == 4 and cd == 33]; db = [t for t, r, cd, a in ev if r == 4 and cd == 35]
+    if ga and da:
+        n = min(len(ga), len(da)); m = min(len(gb), len(db))
+        print("epilogue tile work (median cycles): A", np.median(np.array(da[:n]) - np.array(ga[:n])),
+              "B", np.median(np.array(db[:m]) - np.array(gb[:m])))
     pvA = [t for t, r, cd, a in ev if r == 1 and cd == 10]
     doneA = [t for t, r, cd, a in ev if r == 2 and cd == 21]
     n = min(len(pvA), len(doneA))
