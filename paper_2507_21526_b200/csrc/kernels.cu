@@ -100,13 +100,13 @@ constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
-// instead of MUFU.EX2; 0x11 = 1/4 of the exponentials (MUFU is 16/clk/SM on B200).
+// instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
 #ifndef TA_POLY_MASK
-#define TA_POLY_MASK 0x11
+#define TA_POLY_MASK 0x25
 #endif
 constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_PINGPONG
-#define TA_PINGPONG 1
+#define TA_PINGPONG 0
 #endif
 constexpr bool kPingPong = TA_PINGPONG != 0;
 
@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   uint64_t *exp_turn = q_full + 8;  // [2] softmax ping-pong: tile x may run its exp phase
   uint64_t *l_ready = q_full + 10;  // [2] softmax -> epilogue: row sums / max of an item written
   uint64_t *o_free = q_full + 12;   // [2] epilogue -> MMA: O_x drained from TMEM
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 14);
+  uint64_t *p_hi = q_full + 14;     // [2] P of keys 64..127 written (p_ready: keys 0..63)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 16);
   // cross-warp row reductions of the two column halves of a row:
   // red_max[tile][block parity][half][row]; red_l[item parity][tile][half][row];
   // red_m[item parity][tile][row]
@@ -340,7 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     ptx::mbar_init(q_empty, 1);
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&s_full[x], 1);
-      ptx::mbar_init(&p_ready[x], kHPR * kTileRows);
+      ptx::mbar_init(&p_ready[x], kTileRows);  // first 64 keys of P written
+      ptx::mbar_init(&p_hi[x], kTileRows);     // last 64 keys of P written
       ptx::mbar_init(&o_full[x], 1);
       ptx::mbar_init(&exp_turn[x], 4 * kHPR);  // one arrival per softmax warp of the other tile
       ptx::mbar_init(&l_ready[x], kHPR * kTileRows);
@@ -470,15 +472,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
       };
       // O_x += P_x V_slot; P_x (bf16) lives in the S_x columns; V MN-major (d contiguous).
-      auto issue_pv = [&](int x, uint32_t vslot, const Blk &b, bool acc) {
+      // k-steps [s0, s0 + 4) of the block (keys 16 s .. 16 s + 15)
+      auto issue_pv = [&](int x, uint32_t vslot, const Blk &b, bool acc, int s0) {
         if (!leader) return;
         const uint64_t b0 = dkv_mn + (uint64_t)((vslot * C::kSlotBytes) >> 4);
         const int ksteps = b.ncols / 16;
         const uint32_t pcol = tmem + 128u * x;
-        // P of keys [64h, 64h + 64) sits in TMEM columns [64h, 64h + 32) of S_x (each
-        // column half written over its own S columns by its own softmax warps).
+        // P of keys [64h, 64h + 64) sits in TMEM columns [64h, 64h + 32) of S_x when two
+        // threads share a row (each writes over its own S columns), else in [0, 64).
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
+        for (int s = s0; s < s0 + 4; ++s)
           if (s < ksteps)
             ptx::mma_ts(tmem + 256u + 128u * x,
                         pcol + (s / (8 / kHPR)) * 64 + (s % (8 / kHPR)) * 8,
@@ -537,7 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(10, j);
           const uint32_t kitem = ii - it_beg;  // item of block j
           if (j == 0 && kitem > 0) ptx::mbar_wait(&o_free[0], (kitem - 1) & 1u);  // O_A drained
-          issue_pv(0, vslot, b, j > 0);
+          issue_pv(0, vslot, b, j > 0, 0);   // keys 0..63 while the softmax finishes 64..127
+          ptx::mbar_wait(&p_hi[0], pph[0] ^ 1u);
+          ptx::tc_fence_after();
+          issue_pv(0, vslot, b, j > 0, 4);
           TRACE_MM(11, j);
           if (last) commit(&o_full[0]);
           if (more) {
@@ -561,7 +567,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           ptx::tc_fence_after();
           TRACE_MM(13, j);
           if (j == 0 && kitem > 0) ptx::mbar_wait(&o_free[1], (kitem - 1) & 1u);  // O_B drained
-          issue_pv(1, vslot, b, j > 0);
+          issue_pv(1, vslot, b, j > 0, 0);
+          ptx::mbar_wait(&p_hi[1], pph[1] ^ 1u);
+          ptx::tc_fence_after();
+          issue_pv(1, vslot, b, j > 0, 4);
           TRACE_MM(14, j);
           if (last) commit(&o_full[1]);
           commit(&kv_empty[vslot]);
@@ -751,6 +760,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             pk[e / 2] = ptx::pack_bf16(p0, p1);
           }
           ptx::tmem_st8(tS + c * 8, pk);
+          if (kHPR == 1 && c == 3) {
+            // keys 0..63 of P are in TMEM: the MMA can start PV on them right away
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&p_ready[x]);
+          }
         }
         __syncwarp();
         if (kPingPong && lane == 0) ptx::mbar_arrive(&exp_turn[1 - x]);
@@ -764,7 +779,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&p_ready[x]);
+        ptx::mbar_arrive((kHPR == 2 && hc == 0) ? &p_ready[x] : &p_hi[x]);
         TRACE_SM(21, j);
       }
       // ---------------- hand the item's row statistics to the epilogue warpgroup
