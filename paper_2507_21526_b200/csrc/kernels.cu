@@ -100,9 +100,9 @@ constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
-// instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
+// instead of MUFU.EX2; 0x11 = 1/4 of the exponentials (MUFU is 16/clk/SM on B200).
 #ifndef TA_POLY_MASK
-#define TA_POLY_MASK 0x25
+#define TA_POLY_MASK 0x11
 #endif
 constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_PINGPONG
