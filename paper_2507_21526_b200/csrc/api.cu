@@ -236,6 +236,8 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws,
   const int G = g.group, T = g.tile_tokens;
   if ((s = encode_map(&prm.tm_q, p->q.data, g.n, g.hq, g.d, p->q.stride_head, p->q.stride_token, T, G)))
     return s;
+  if ((s = encode_map(&prm.tm_o, p->o.data, g.n, g.hq, g.d, p->o.stride_head, p->o.stride_token, T, G)))
+    return s;
   if ((s = encode_map(&prm.tm_k, p->k.data, g.n, g.hkv, g.d, p->k.stride_head, p->k.stride_token,
                       ta::kBlockKeys, 1)))
     return s;

@@ -19,6 +19,7 @@ struct alignas(64) AttnParams {
   CUtensorMap tm_vs; // V sink rows
   CUtensorMap tm_kb; // K band rows of a fused first block: box {64, 112, 1}
   CUtensorMap tm_vb; // V, same
+  CUtensorMap tm_o;  // O [Hq][N][d] (bf16 output, epilogue TMA store): box {64, T, G}
   void *o;           // bf16 O [Hq][N][d] with element strides below
   int64_t o_sh, o_st;
   float *lse;        // optional [Hq][N]

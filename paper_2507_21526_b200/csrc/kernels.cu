@@ -67,7 +67,7 @@ struct Cfg {
   static constexpr int kStages = (D == 128) ? 4 : 8;
   static constexpr int kBarBytes = 1024;
   static constexpr int kRedBytes = 2 * 2 * 2 * kTileRows * 4 * 2 + 2 * 2 * kTileRows * 4;
-  static constexpr int kStageBytes = 8 * 1024;  // epilogue transpose: 1 KB per epilogue warp (<= 8)
+  static constexpr int kStageBytes = 128 * 128;  // epilogue: one 64-column half of an O tile (bf16, SW128)
   static constexpr int kSmem = 1024 /*align slack*/ + 2 * kQTileBytes + kStages * kSlotBytes +
                                kBarBytes + kRedBytes + kStageBytes;
 };
@@ -100,9 +100,9 @@ constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
-// instead of MUFU.EX2; 0x11 = 1/4 of the exponentials (MUFU is 16/clk/SM on B200).
+// instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
 #ifndef TA_POLY_MASK
-#define TA_POLY_MASK 0x11
+#define TA_POLY_MASK 0x25
 #endif
 constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_PINGPONG
@@ -254,11 +254,6 @@ __device__ __forceinline__ uint32_t iv_bits(int lo, int hi) {
   return upto_hi & ~((1u << lo) - 1u);
 }
 
-// Warp-level barrier with shared-memory ordering that ptxas cannot elide.
-__device__ __forceinline__ void ptx_fence_warp() {
-  asm volatile("bar.warp.sync 0xffffffff;" ::: "memory");
-  asm volatile("fence.acq_rel.cta;" ::: "memory");
-}
 
 __device__ __forceinline__ void sts_f32(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
@@ -272,18 +267,7 @@ __device__ __forceinline__ void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint3
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w)
                : "memory");
 }
-__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
-  uint4 v;
-  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(a)
-               : "memory");
-  return v;
-}
 
-__device__ __forceinline__ void stg_v4(uint64_t a, uint4 v) {
-  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
 
 // 256-bit global store (STG.E.256 on sm_100a); p must be 32-byte aligned.
 __device__ __forceinline__ void st_global_v8(void *p, const uint32_t *v) {
@@ -327,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   float *red_max = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bars) + C::kBarBytes);
   float *red_l = red_max + 2 * 2 * 2 * kTileRows;
   float *red_m = red_l + 2 * 2 * 2 * kTileRows;
-  uint8_t *stage = reinterpret_cast<uint8_t *>(red_m + 2 * 2 * kTileRows);  // [4 epilogue warps][1 KB]
+  uint8_t *stage = reinterpret_cast<uint8_t *>(red_m + 2 * 2 * kTileRows);  // 1024-aligned, 16 KB
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -607,7 +591,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     // shared-space addresses (explicit st.shared / ld.shared, not generic accesses)
     const uint32_t my_max_s = ptx::smem_u32(red_max + (x * 2 * 2 + hc) * kTileRows + r);
     const uint32_t peer_max_s = ptx::smem_u32(red_max + (x * 2 * 2 + (1 - hc)) * kTileRows + r);
-    const uint32_t stg_s = ptx::smem_u32(stage + warp * 1024);
     uint32_t sph = 0, ecount = 0, kitem_sm = 0;
 #ifdef TA_TRACE
     uint32_t trc = 0;
@@ -807,7 +790,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     const bool row_in_tile = r < p.group * T;
     const int hoff = row_in_tile ? r / T : 0;
     const int toff = row_in_tile ? r % T : 0;
-    const uint32_t stg_s = ptx::smem_u32(stage + (warp - kEpiWarp0) * 1024);
     uint32_t kitem = 0;
 #ifdef TA_TRACE
     uint32_t trc = 0;
@@ -848,12 +830,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           p.part_lse[prow] = lse;
         } else {
           const int head = f.kvh * p.group + hoff;
-          const uint64_t row_addr = reinterpret_cast<uint64_t>(reinterpret_cast<__nv_bfloat16 *>(p.o) +
-                                                               (int64_t)head * p.o_sh + (int64_t)tok * p.o_st);
-          const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-          // 64 columns (128 B of bf16) per pass; coalesced stores through a 1 KB transpose:
-          // 8 rows per round are staged (XOR-swizzled 16-byte pieces), then each STG.128
-          // covers 4 rows x 128 B instead of 32 rows x 16 B.
+          // O tile -> bf16 -> smem (128 rows x 64 columns per pass, 128B-swizzled like the Q
+          // tile) -> one TMA tensor store of box {64, T, G}: the same GQA-packed box the Q
+          // tile was loaded with, so rows beyond G*T or tokens >= N are clipped by TMA.
+          const uint32_t stage_s = ptx::smem_u32(stage);
 #pragma unroll 1
           for (int hb = 0; hb < D / 64; ++hb) {
             uint32_t pk[32];
@@ -867,32 +847,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 pk[c * 8 + e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv,
                                                __uint_as_float(ov[2 * e + 1]) * inv);
             }
-#ifndef TA_EPI_TRANSPOSE
-            if (valid)
+            // staging buffer free: the previous TMA store has finished reading it
+            if (threadIdx.x == kEpiWarp0 * 32) ptx::bulk_wait_read0();
+            asm volatile("bar.sync 5, 128;" ::: "memory");
 #pragma unroll
-              for (int pc = 0; pc < 8; ++pc)
-                stg_v4(row_addr + hb * 128 + (pc << 4), make_uint4(pk[4 * pc], pk[4 * pc + 1], pk[4 * pc + 2], pk[4 * pc + 3]));
-            if (false)
-#endif
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if ((lane >> 3) == q) {
-                const int rr = lane & 7;
-#pragma unroll
-                for (int pc = 0; pc < 8; ++pc)
-                  sts_v4(stg_s + rr * 128 + ((pc ^ rr) << 4), pk[4 * pc], pk[4 * pc + 1],
-                         pk[4 * pc + 2], pk[4 * pc + 3]);
-              }
-              ptx_fence_warp();
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int rr = h * 4 + (lane >> 3), pc = lane & 7;
-                const uint4 v4 = lds_v4(stg_s + rr * 128 + ((pc ^ rr) << 4));
-                const int row = q * 8 + rr;  // warp-local row whose piece this lane stores
-                const uint64_t a = __shfl_sync(0xffffffffu, row_addr, row);
-                if ((vmask >> row) & 1u) stg_v4(a + hb * 128 + (pc << 4), v4);
-              }
-              ptx_fence_warp();
+            for (int pc = 0; pc < 8; ++pc)
+              sts_v4(stage_s + r * 128 + ((pc ^ (r & 7)) << 4), pk[4 * pc], pk[4 * pc + 1],
+                     pk[4 * pc + 2], pk[4 * pc + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 5, 128;" ::: "memory");
+            if (threadIdx.x == kEpiWarp0 * 32) {
+              ptx::tma_store_3d(&p.tm_o, stage, hb * 64, f.r0 + x * T, f.kvh * p.group);
+              ptx::bulk_commit();
             }
           }
           if (valid && p.lse) p.lse[(int64_t)head * p.n + tok] = lse;
@@ -905,6 +871,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       }
     }
   }
+  if (threadIdx.x == kEpiWarp0 * 32) ptx::bulk_wait0();  // epilogue TMA stores complete
   __syncthreads();
   if (warp == kAllocWarp) {
     ptx::tc_fence_after();
