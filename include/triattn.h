@@ -1,4 +1,4 @@
-/* triattn.h -- C ABI v1 of the B200-native TriangleMix prefill-attention library.
+/* triattn.h -- C ABI v2 of the B200-native TriangleMix prefill-attention library.
  *
  * The library computes, for one prefill request (batch 1) and one attention
  * layer, the masked softmax attention of PAPER.md section 2.1
@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define TA_ABI_VERSION 1
+#define TA_ABI_VERSION 2  /* v2: last_q = 0 (StreamingMix), final-layer last-rows entry points */
 
 /* Same type as the CUDA runtime's cudaStream_t (a duplicate identical typedef is
  * legal in C11/C++), so callers need no CUDA headers. NULL = legacy stream. */
@@ -54,8 +54,9 @@ typedef enum {
   TA_ERR_EMPTY_SEQUENCE = 2, /* seq_len == 0                       (SPEC EmptySequence S:L56)   */
   TA_ERR_SHAPE = 3,          /* heads < 1, Hq % Hkv != 0, seq_len < 0, stride too small
                                 (SPEC ShapeError S:L168)                                        */
-  TA_ERR_PARAMS = 4,         /* sink < 0, window < 1, last_q < 1, tri_start < 0, layer < 0
-                                (TriangleParams invariants S:L39-41; "last >= 1")       */
+  TA_ERR_PARAMS = 4,         /* sink < 0, window < 1, last_q < 0 (< 1 for the last-rows
+                                entry points), tri_start < 0, layer < 0, num_ctas < 1
+                                (TriangleParams invariants S:L39-41)                            */
   TA_ERR_UNSUPPORTED = 5,    /* head_dim not in {64,128}; Hq/Hkv > 128; seq_len >= 2^31;
                                 pointer not 16-byte aligned; stride*2 not a multiple of 16;
                                 device is not sm_100                                             */
@@ -91,7 +92,9 @@ typedef struct {
 typedef struct {
   int32_t sink;   /* si >= 0 sink key columns  j < si */
   int32_t window; /* sl >= 1 sliding-window keys  i - j < sl, incl. i */
-  int32_t last_q; /* last >= 1 final query rows  i >= N - last */
+  int32_t last_q; /* last >= 0 final query rows  i >= N - last;
+                     0 = no Last Q-K section: the StreamingMix pattern of the paper's
+                     baselines (reading R12)                          */
 } ta_triangle;
 
 /* Bytes of device workspace triangle_attn_prefill / dense_attn_prefill need
@@ -120,6 +123,20 @@ ta_status ta_layer_attn_prefill(int32_t layer, int32_t tri_start, const ta_probl
                                 const ta_triangle *tri, void *ws, size_t ws_bytes,
                                 cudaStream_t stream);
 
+/* ---- final layer: last query rows only ----------------------- *
+ * "For the last layer, only the last r rows of the attention output are needed"
+ * (TriangleMix section 2.4): O_last = Softmax(Q_last K^T * scale) V over ALL causal keys
+ * of the last r = min(last_q, N) query rows, last_q >= 1.  Runs only the split-K
+ * LASTQ items of those rows (chunks of [0, i]) and the LSE merge
+ * (P:L641-642); no streaming pass.
+ *   p->q, k, v: as for the other calls ([heads][N][d]).
+ *   p->o:   Hq heads x r ROWS: O row t holds query token N - r + t.
+ *   p->lse: optional [Hq][r] fp32, same row convention.
+ * ws: >= ta_last_rows_workspace_size(p, last_q) bytes, 256-B aligned. */
+size_t ta_last_rows_workspace_size(const ta_problem *p, int32_t last_q);
+ta_status last_rows_attn_prefill(const ta_problem *p, int32_t last_q, void *ws, size_t ws_bytes,
+                                 cudaStream_t stream);
+
 /* ---- introspection (host only; no GPU needed) ---------------------------- */
 
 /* Kept (i, j) pairs per head of the mask (tri == NULL -> dense causal).
@@ -133,6 +150,9 @@ ta_status ta_pair_count(int64_t seq_len, const ta_triangle *tri, int64_t *out_pa
  * *inout_bytes set to the size needed. */
 ta_status ta_schedule_export(const ta_problem *p, const ta_triangle *tri, int32_t num_ctas,
                              void *host_buf, size_t *inout_bytes);
+/* Same for the final-layer last-rows mode (header kind field 2). */
+ta_status ta_last_rows_schedule_export(const ta_problem *p, int32_t last_q, int32_t num_ctas,
+                                       void *host_buf, size_t *inout_bytes);
 
 const char *ta_status_str(ta_status s);
 /* Detail of this thread's last non-OK return ("" if none). */

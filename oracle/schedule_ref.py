@@ -7,7 +7,10 @@ items cover every kept (row, key) pair of the mask exactly once.
 
 Spec summary:
   G = Hq/Hkv, T = 128 // G, P = 2T tokens per item ("pair"), pairs = ceil(N/P).
-  triangle: p_last0 = max(0, N-last) // P; pairs p >= p_last0 are LAST pairs.
+  triangle: p_last0 = max(0, N-last) // P (= pairs when last = 0: StreamingMix has no
+    last rows); pairs p >= p_last0 are LAST pairs.
+  last_rows (final-layer mode): si = 0, sl = 1, last = min(last, N); only the
+    LASTQ items of the last pairs (no STREAM items); header kind field 2.
     STREAM(kvh, p), p < p_last0: band [max(si, r0-sl+1), r1+1) (empty -> [r1+1, r1+1));
        sink [0, min(si, r1+1)) implicit.
     LASTQ(kvh, p, c): [c*ck, min((c+1)*ck, r1+1)) for c < ceil((r1+1)/ck).
@@ -42,18 +45,21 @@ def blocks_of(kb, ke):
     return out
 
 
-def geometry(n, hq, hkv, d, si, sl, last, dense):
+def geometry(n, hq, hkv, d, si, sl, last, dense, last_rows=False):
     g = hq // hkv
     t = 128 // g
     p = 2 * t
     pairs = -(-n // p)
+    last_rows = bool(last_rows) and not dense
     if dense:
         si, sl, last = 0, 1, 1
         p_last0 = pairs
     else:
-        p_last0 = max(0, n - last) // p
-    return dict(n=n, hq=hq, hkv=hkv, d=d, si=si, sl=sl, last=last, dense=dense, G=g, T=t, P=p,
-                pairs=pairs, p_last0=p_last0)
+        if last_rows:
+            si, sl, last = 0, 1, min(last, n)
+        p_last0 = pairs if last == 0 else max(0, n - last) // p
+    return dict(n=n, hq=hq, hkv=hkv, d=d, si=si, sl=sl, last=last, dense=dense, last_rows=last_rows,
+                G=g, T=t, P=p, pairs=pairs, p_last0=p_last0)
 
 
 def rows(geo, p):
@@ -97,7 +103,7 @@ def chunk_keys(geo, num_ctas):
     if geo["dense"]:
         return 0
     tot = 0
-    for p in range(geo["p_last0"]):
+    for p in range(0 if geo["last_rows"] else geo["p_last0"]):
         tot += cost(geo, stream_item(geo, 0, p))
     for p in range(geo["p_last0"], geo["pairs"]):
         tot += cost(geo, (LASTQ, 0, p, 0, rows(geo, p)[1] + 1))
@@ -121,15 +127,16 @@ def enumerate_items(geo, ck):
             span = rows(geo, p)[1] + 1
             for c in range(-(-span // ck)):
                 items.append((LASTQ, kvh, p, c * ck, min((c + 1) * ck, span)))
-    for kvh in range(geo["hkv"]):
-        for p in range(geo["p_last0"]):
-            items.append(stream_item(geo, kvh, p))
+    if not geo["last_rows"]:
+        for kvh in range(geo["hkv"]):
+            for p in range(geo["p_last0"]):
+                items.append(stream_item(geo, kvh, p))
     return items
 
 
-def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas):
+def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False):
     """Returns (geo, ck, s_max, per_cta_lists)."""
-    geo = geometry(n, hq, hkv, d, si, sl, last, dense)
+    geo = geometry(n, hq, hkv, d, si, sl, last, dense, last_rows)
     ck = chunk_keys(geo, num_ctas)
     s_max = 0 if dense else -(-n // ck)
     items = enumerate_items(geo, ck)
@@ -144,10 +151,11 @@ def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas):
     return geo, ck, s_max, per, load
 
 
-def serialize(n, hq, hkv, d, si, sl, last, dense, num_ctas) -> bytes:
-    geo, ck, s_max, per, _ = schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas)
+def serialize(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False) -> bytes:
+    geo, ck, s_max, per, _ = schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows)
     nitems = sum(len(x) for x in per)
-    hdr = [MAGIC, VERSION, 1 if dense else 0, n, hq, hkv, d, geo["si"], geo["sl"], geo["last"],
+    kind = 1 if dense else (2 if geo["last_rows"] else 0)
+    hdr = [MAGIC, VERSION, kind, n, hq, hkv, d, geo["si"], geo["sl"], geo["last"],
            geo["T"], 2, ck, num_ctas, nitems, s_max]
     out = struct.pack("<16I", *hdr)
     off = [0]

@@ -11,6 +11,7 @@ Function names follow the C ABI:
     triangle_attn_prefill(q, k, v, sink=8, window=512, last_q=128)   # deep layers
     dense_attn_prefill(q, k, v)                                      # shallow layers
     layer_attn_prefill(layer, tri_start, q, k, v, ...)               # TriangleMix rule
+    last_rows_attn_prefill(q, k, v, last_q=128)                      # final layer, last rows
     pair_count(seq_len, sink, window, last_q) / schedule_export(...) # introspection
 
 q: [Hq][N][d] bf16 CUDA tensor view (any strides with unit d-stride), k/v:
@@ -24,7 +25,8 @@ import os
 __all__ = [
     "TriattnError", "triangle_attn_prefill", "dense_attn_prefill", "layer_attn_prefill",
     "workspace_size", "pair_count", "schedule_export", "abi_version", "release_caches",
-    "library_path", "STATUS", "profile_begin", "profile_end",
+    "library_path", "STATUS", "profile_begin", "profile_end", "last_rows_attn_prefill",
+    "last_rows_workspace_size", "last_rows_schedule_export",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -87,6 +89,12 @@ def _load():
     lib.ta_pair_count.restype = ctypes.c_int
     lib.ta_schedule_export.argtypes = [P, Tp, ctypes.c_int32, vp, ctypes.POINTER(sz)]
     lib.ta_schedule_export.restype = ctypes.c_int
+    lib.ta_last_rows_workspace_size.argtypes = [P, ctypes.c_int32]
+    lib.ta_last_rows_workspace_size.restype = sz
+    lib.last_rows_attn_prefill.argtypes = [P, ctypes.c_int32, vp, sz, vp]
+    lib.last_rows_attn_prefill.restype = ctypes.c_int
+    lib.ta_last_rows_schedule_export.argtypes = [P, ctypes.c_int32, ctypes.c_int32, vp, ctypes.POINTER(sz)]
+    lib.ta_last_rows_schedule_export.restype = ctypes.c_int
     lib.ta_status_str.argtypes = [ctypes.c_int]
     lib.ta_status_str.restype = ctypes.c_char_p
     lib.ta_last_error.argtypes = []
@@ -125,24 +133,28 @@ def _problem(q, k, v, o, lse, scale):
     return p
 
 
-def _check_tensors(q, k, v, o, lse):
+def _check_tensors(q, k, v, o, lse, o_rows=None):
     import torch
     for name, t in (("q", q), ("k", k), ("v", v), ("o", o)):
         if t.dtype != torch.bfloat16 or t.dim() != 3 or not t.is_cuda or t.stride(2) != 1:
             raise TriattnError(3, f"{name}: need a CUDA bf16 [heads][tokens][d] view, d-stride 1")
-    if k.shape != v.shape or q.shape[1:] != k.shape[1:] or o.shape != q.shape:
+    rows = q.shape[1] if o_rows is None else o_rows
+    if k.shape != v.shape or q.shape[1:] != k.shape[1:] or tuple(o.shape) != (q.shape[0], rows, q.shape[2]):
         raise TriattnError(3, "q/k/v/o shapes disagree")
     if lse is not None and (lse.dtype != torch.float32 or not lse.is_contiguous()
-                            or tuple(lse.shape) != (q.shape[0], q.shape[1])):
-        raise TriattnError(3, "lse must be contiguous fp32 [Hq][N]")
+                            or tuple(lse.shape) != (q.shape[0], rows)):
+        raise TriattnError(3, "lse must be contiguous fp32 [Hq][rows of o]")
 
 
 _ws_cache: dict = {}
 
 
-def _workspace(p, tri, device):
+def _workspace(p, tri, device, last_rows=None):
     import torch
-    need = _load().ta_workspace_size(ctypes.byref(p), ctypes.byref(tri) if tri is not None else None)
+    if last_rows is not None:
+        need = _load().ta_last_rows_workspace_size(ctypes.byref(p), int(last_rows))
+    else:
+        need = _load().ta_workspace_size(ctypes.byref(p), ctypes.byref(tri) if tri is not None else None)
     if need == 0:
         return None, 0
     key = (device.index, need)
@@ -203,6 +215,39 @@ def layer_attn_prefill(layer: int, tri_start: int, q, k, v, o=None, *, sink: int
     _check(_load().ta_layer_attn_prefill(layer, tri_start, ctypes.byref(p), ctypes.byref(tri), ws,
                                          need, _stream(stream)))
     return o
+
+
+def last_rows_attn_prefill(q, k, v, o=None, *, last_q: int = 128, lse=None, scale: float = 0.0,
+                           stream=None):
+    """Final-layer attention of the last r = min(last_q, N) query rows only:
+    o[h, t] = softmax over all causal keys of query N - r + t.  Returns o [Hq][r][d]."""
+    import torch
+    r = min(int(last_q), q.shape[1]) if last_q >= 1 else int(last_q)
+    if o is None:
+        o = torch.empty((q.shape[0], max(r, 0), q.shape[2]), dtype=q.dtype, device=q.device)
+    _check_tensors(q, k, v, o, lse, o_rows=max(r, 0))
+    p = _problem(q, k, v, o, lse, scale)
+    ws, need = _workspace(p, None, q.device, last_rows=last_q)
+    _check(_load().last_rows_attn_prefill(ctypes.byref(p), int(last_q), ws, need, _stream(stream)))
+    return o
+
+
+def last_rows_workspace_size(seq_len: int, hq: int, hkv: int, d: int, last_q: int = 128) -> int:
+    p = _shape_problem(seq_len, hq, hkv, d)
+    return int(_load().ta_last_rows_workspace_size(ctypes.byref(p), int(last_q)))
+
+
+def last_rows_schedule_export(seq_len: int, hq: int, hkv: int, d: int, num_ctas: int,
+                              last_q: int = 128) -> bytes:
+    p = _shape_problem(seq_len, hq, hkv, d)
+    n = ctypes.c_size_t(0)
+    lib = _load()
+    st = lib.ta_last_rows_schedule_export(ctypes.byref(p), int(last_q), num_ctas, None, ctypes.byref(n))
+    if st not in (0, 6):
+        _check(st)
+    buf = ctypes.create_string_buffer(n.value)
+    _check(lib.ta_last_rows_schedule_export(ctypes.byref(p), int(last_q), num_ctas, buf, ctypes.byref(n)))
+    return buf.raw[: n.value]
 
 
 def _shape_problem(seq_len, hq, hkv, d):

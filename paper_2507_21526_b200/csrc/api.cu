@@ -32,7 +32,7 @@ ta_status validate_triangle(const ta_triangle *t) {
   if (!t) return fail(TA_ERR_NULL_ARG, "triangle parameters are NULL");
   if (t->sink < 0) return fail(TA_ERR_PARAMS, "sink < 0 (S:L39)");
   if (t->window < 1) return fail(TA_ERR_PARAMS, "window < 1 (S:L39)");
-  if (t->last_q < 1) return fail(TA_ERR_PARAMS, "last_q < 1 (P:L161 'last >= 1')");
+  if (t->last_q < 0) return fail(TA_ERR_PARAMS, "last_q < 0 (0 = StreamingMix, reading R12)");
   return TA_OK;
 }
 
@@ -71,18 +71,20 @@ ta_status validate_tensor(const char *name, const void *data, int64_t sh, int64_
   return TA_OK;
 }
 
-ta_status validate_problem(const ta_problem *p) {
+// o_rows: token rows of the O view (N, or the last_q rows of the final-layer mode)
+ta_status validate_problem(const ta_problem *p, int64_t o_rows = -1) {
   ta_status s = validate_shape(p);
   if (s != TA_OK) return s;
   const int64_t n = p->seq_len;
   const int d = p->head_dim;
+  if (o_rows < 0) o_rows = n;
   if ((s = validate_tensor("q", p->q.data, p->q.stride_head, p->q.stride_token, p->num_q_heads, n, d)))
     return s;
   if ((s = validate_tensor("k", p->k.data, p->k.stride_head, p->k.stride_token, p->num_kv_heads, n, d)))
     return s;
   if ((s = validate_tensor("v", p->v.data, p->v.stride_head, p->v.stride_token, p->num_kv_heads, n, d)))
     return s;
-  if ((s = validate_tensor("o", p->o.data, p->o.stride_head, p->o.stride_token, p->num_q_heads, n, d)))
+  if ((s = validate_tensor("o", p->o.data, p->o.stride_head, p->o.stride_token, p->num_q_heads, o_rows, d)))
     return s;
   return TA_OK;
 }
@@ -95,7 +97,7 @@ struct DevSchedule {
   int num_ctas = 0;
 };
 
-typedef std::tuple<int, int64_t, int, int, int, int, int, int, int, int> SchedKey;
+typedef std::tuple<int, int64_t, int, int, int, int, int, int, int, int, int> SchedKey;
 std::mutex g_mu;
 std::map<SchedKey, DevSchedule> g_sched;
 
@@ -129,7 +131,8 @@ ta_status device_info(int *dev, DeviceInfo *info) {
 }
 
 ta_status get_schedule(int dev, const ta::Geometry &g, int num_ctas, DevSchedule *out) {
-  SchedKey key(dev, g.n, g.hq, g.hkv, g.d, g.dense ? 1 : 0, g.si, g.sl, g.last, num_ctas);
+  SchedKey key(dev, g.n, g.hq, g.hkv, g.d, g.dense ? 1 : 0, g.last_only ? 1 : 0, g.si, g.sl, g.last,
+               num_ctas);
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_sched.find(key);
   if (it != g_sched.end()) {
@@ -207,20 +210,35 @@ cudaEvent_t take_event() {
   return e;
 }
 
-ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws, size_t ws_bytes,
-              cudaStream_t stream) {
-  ta_status s = validate_problem(p);
+enum Mode { kTriangle, kDenseMode, kLastRows };
+
+// Geometry of a call: triangle (tri), dense, or the final-layer last-rows mode (last_q rows).
+bool call_geometry(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t last_q,
+                   ta::Geometry *g, std::string *err) {
+  const bool dense = mode == kDenseMode;
+  if (mode == kLastRows)
+    return ta::make_geometry(p->seq_len, p->num_q_heads, p->num_kv_heads, p->head_dim, false, 0, 1,
+                             last_q, g, err, true);
+  return ta::make_geometry(p->seq_len, p->num_q_heads, p->num_kv_heads, p->head_dim, dense,
+                           dense ? 0 : tri->sink, dense ? 1 : tri->window, dense ? 1 : tri->last_q, g,
+                           err);
+}
+
+ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t last_q, void *ws,
+              size_t ws_bytes, cudaStream_t stream) {
+  const bool dense = mode == kDenseMode;
+  ta_status s = validate_shape(p);
   if (s != TA_OK) return s;
-  if (!dense && (s = validate_triangle(tri)) != TA_OK) return s;
+  if (mode == kLastRows && last_q < 1) return fail(TA_ERR_PARAMS, "last_q < 1 (final-layer rows)");
+  const int64_t o_rows = mode == kLastRows ? std::min<int64_t>(last_q, p->seq_len) : p->seq_len;
+  if ((s = validate_problem(p, o_rows)) != TA_OK) return s;
+  if (mode == kTriangle && (s = validate_triangle(tri)) != TA_OK) return s;
   int dev;
   DeviceInfo di;
   if ((s = device_info(&dev, &di)) != TA_OK) return s;
   ta::Geometry g;
   std::string err;
-  if (!ta::make_geometry(p->seq_len, p->num_q_heads, p->num_kv_heads, p->head_dim, dense,
-                         dense ? 0 : tri->sink, dense ? 1 : tri->window, dense ? 1 : tri->last_q,
-                         &g, &err))
-    return fail(TA_ERR_SHAPE, err);
+  if (!call_geometry(p, tri, mode, last_q, &g, &err)) return fail(TA_ERR_SHAPE, err);
   ta::plan_chunks(&g, di.sms);
   const size_t need = ta::workspace_bytes(g);
   if (need > 0) {
@@ -236,7 +254,7 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws,
   const int G = g.group, T = g.tile_tokens;
   if ((s = encode_map(&prm.tm_q, p->q.data, g.n, g.hq, g.d, p->q.stride_head, p->q.stride_token, T, G)))
     return s;
-  if ((s = encode_map(&prm.tm_o, p->o.data, g.n, g.hq, g.d, p->o.stride_head, p->o.stride_token, T, G)))
+  if ((s = encode_map(&prm.tm_o, p->o.data, o_rows, g.hq, g.d, p->o.stride_head, p->o.stride_token, T, G)))
     return s;
   if ((s = encode_map(&prm.tm_k, p->k.data, g.n, g.hkv, g.d, p->k.stride_head, p->k.stride_token,
                       ta::kBlockKeys, 1)))
@@ -277,6 +295,8 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws,
   prm.sl = g.sl;
   prm.last = g.last;
   prm.dense = dense ? 1 : 0;
+  prm.last_only = g.last_only ? 1 : 0;
+  prm.o_row0 = (int)(g.n - o_rows);
   prm.p_last0 = (int)ds.g.p_last0;
   prm.n_last_pairs = (int)ds.g.n_last_pairs;
   prm.chunk_keys = ds.g.chunk_keys;
@@ -319,13 +339,12 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, bool dense, void *ws,
   return TA_OK;
 }
 
-size_t ws_size(const ta_problem *p, const ta_triangle *tri) {
+size_t ws_size(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t last_q) {
   if (validate_shape(p) != TA_OK) return 0;
-  if (tri && validate_triangle(tri) != TA_OK) return 0;
+  if (mode == kTriangle && (!tri || validate_triangle(tri) != TA_OK)) return 0;
+  if (mode == kLastRows && last_q < 1) return 0;
   ta::Geometry g;
-  if (!ta::make_geometry(p->seq_len, p->num_q_heads, p->num_kv_heads, p->head_dim, tri == nullptr,
-                         tri ? tri->sink : 0, tri ? tri->window : 1, tri ? tri->last_q : 1, &g, nullptr))
-    return 0;
+  if (!call_geometry(p, tri, mode, last_q, &g, nullptr)) return 0;
   int sms = 148;  // B200; used when no device is visible (host-only callers)
   int dev;
   if (cudaGetDevice(&dev) == cudaSuccess) {
@@ -344,7 +363,7 @@ extern "C" {
 
 size_t ta_workspace_size(const ta_problem *p, const ta_triangle *tri) {
   try {
-    return ws_size(p, tri);
+    return ws_size(p, tri, tri ? kTriangle : kDenseMode, 0);
   } catch (...) {
     return 0;
   }
@@ -354,7 +373,7 @@ ta_status triangle_attn_prefill(const ta_problem *p, const ta_triangle *tri, voi
                                 size_t ws_bytes, cudaStream_t stream) {
   try {
     if (!tri) return fail(TA_ERR_NULL_ARG, "triangle parameters are NULL");
-    return run(p, tri, false, ws, ws_bytes, stream);
+    return run(p, tri, kTriangle, 0, ws, ws_bytes, stream);
   } catch (const std::exception &ex) {
     return fail(TA_ERR_CUDA, ex.what());
   } catch (...) {
@@ -364,7 +383,7 @@ ta_status triangle_attn_prefill(const ta_problem *p, const ta_triangle *tri, voi
 
 ta_status dense_attn_prefill(const ta_problem *p, void *ws, size_t ws_bytes, cudaStream_t stream) {
   try {
-    return run(p, nullptr, true, ws, ws_bytes, stream);
+    return run(p, nullptr, kDenseMode, 0, ws, ws_bytes, stream);
   } catch (const std::exception &ex) {
     return fail(TA_ERR_CUDA, ex.what());
   } catch (...) {
@@ -402,19 +421,19 @@ ta_status ta_pair_count(int64_t seq_len, const ta_triangle *tri, int64_t *out) {
   return TA_OK;
 }
 
-ta_status ta_schedule_export(const ta_problem *p, const ta_triangle *tri, int32_t num_ctas,
-                             void *host_buf, size_t *inout_bytes) {
+namespace {
+ta_status export_schedule(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t last_q,
+                          int32_t num_ctas, void *host_buf, size_t *inout_bytes) {
   try {
     if (!inout_bytes) return fail(TA_ERR_NULL_ARG, "inout_bytes is NULL");
     ta_status s = validate_shape(p);
     if (s != TA_OK) return s;
-    if (tri && (s = validate_triangle(tri)) != TA_OK) return s;
+    if (mode == kTriangle && (s = validate_triangle(tri)) != TA_OK) return s;
+    if (mode == kLastRows && last_q < 1) return fail(TA_ERR_PARAMS, "last_q < 1 (final-layer rows)");
     if (num_ctas < 1) return fail(TA_ERR_PARAMS, "num_ctas < 1");
     ta::Geometry g;
     std::string err;
-    if (!ta::make_geometry(p->seq_len, p->num_q_heads, p->num_kv_heads, p->head_dim, tri == nullptr,
-                           tri ? tri->sink : 0, tri ? tri->window : 1, tri ? tri->last_q : 1, &g, &err))
-      return fail(TA_ERR_SHAPE, err);
+    if (!call_geometry(p, tri, mode, last_q, &g, &err)) return fail(TA_ERR_SHAPE, err);
     std::vector<uint8_t> bytes = ta::serialize(ta::build_schedule(g, num_ctas));
     const size_t cap = *inout_bytes;
     *inout_bytes = bytes.size();
@@ -424,6 +443,36 @@ ta_status ta_schedule_export(const ta_problem *p, const ta_triangle *tri, int32_
   } catch (...) {
     return fail(TA_ERR_CUDA, "exception in ta_schedule_export");
   }
+}
+}  // namespace
+
+ta_status ta_schedule_export(const ta_problem *p, const ta_triangle *tri, int32_t num_ctas,
+                             void *host_buf, size_t *inout_bytes) {
+  return export_schedule(p, tri, tri ? kTriangle : kDenseMode, 0, num_ctas, host_buf, inout_bytes);
+}
+
+size_t ta_last_rows_workspace_size(const ta_problem *p, int32_t last_q) {
+  try {
+    return ws_size(p, nullptr, kLastRows, last_q);
+  } catch (...) {
+    return 0;
+  }
+}
+
+ta_status last_rows_attn_prefill(const ta_problem *p, int32_t last_q, void *ws, size_t ws_bytes,
+                                 cudaStream_t stream) {
+  try {
+    return run(p, nullptr, kLastRows, last_q, ws, ws_bytes, stream);
+  } catch (const std::exception &ex) {
+    return fail(TA_ERR_CUDA, ex.what());
+  } catch (...) {
+    return fail(TA_ERR_CUDA, "unknown exception");
+  }
+}
+
+ta_status ta_last_rows_schedule_export(const ta_problem *p, int32_t last_q, int32_t num_ctas,
+                                       void *host_buf, size_t *inout_bytes) {
+  return export_schedule(p, nullptr, kLastRows, last_q, num_ctas, host_buf, inout_bytes);
 }
 
 const char *ta_status_str(ta_status s) {

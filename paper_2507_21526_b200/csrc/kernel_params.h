@@ -22,13 +22,15 @@ struct alignas(64) AttnParams {
   CUtensorMap tm_o;  // O [Hq][N][d] (bf16 output, epilogue TMA store): box {64, T, G}
   void *o;           // bf16 O [Hq][N][d] with element strides below
   int64_t o_sh, o_st;
-  float *lse;        // optional [Hq][N]
+  float *lse;        // optional [Hq][N - o_row0]
   float *part_o;     // split-K partials [slot][2*128 rows][d] fp32 (normalised O_c)
   float *part_lse;   // [slot][2*128 rows] fp32 natural-log LSE_c
   const Item *items;
   const uint32_t *offsets;
   int n, hq, group, tile_tokens, pair_tokens;
   int si, sl, last, dense;
+  int last_only;     // final-layer mode: the merge writes only rows >= N - last ...
+  int o_row0;        // ... into O / lse whose row 0 is token o_row0 (0 otherwise)
   int p_last0, n_last_pairs, chunk_keys, s_max;
   float scale_log2;  // softmax_scale * log2(e)
   float scale;       // softmax_scale

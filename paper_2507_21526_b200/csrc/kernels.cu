@@ -101,6 +101,9 @@ constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
 // instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
+#ifndef TA_POLY_DEG
+#define TA_POLY_DEG 3
+#endif
 #ifndef TA_POLY_MASK
 #define TA_POLY_MASK 0x25
 #endif
@@ -229,8 +232,13 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float &y0, float 
   const uint64_t t = fadd2(x, f2pack(kMagic, kMagic));
   const uint64_t r = fadd2(t, f2pack(-kMagic, -kMagic));
   uint64_t f = ffma2(r, f2pack(-1.f, -1.f), x);    // x - rint(x), exact
-  uint64_t pp = ffma2(f, f2pack(0.055008627f, 0.055008627f), f2pack(0.24221043f, 0.24221043f));
-  pp = ffma2(pp, f, f2pack(0.69328302f, 0.69328302f));
+  uint64_t pp;
+  if (TA_POLY_DEG == 3) {
+    pp = ffma2(f, f2pack(0.055008280f, 0.055008280f), f2pack(0.24220959f, 0.24220959f));
+    pp = ffma2(pp, f, f2pack(0.69328285f, 0.69328285f));
+  } else {  // degree 2: max rel. err 2.0e-3 (about the bf16 rounding of P)
+    pp = ffma2(f, f2pack(0.23985499f, 0.23985499f), f2pack(0.70292904f, 0.70292904f));
+  }
   pp = ffma2(pp, f, f2pack(1.0f, 1.0f));
   float p0, p1, t0, t1;
   f2unpack(pp, p0, p1);
@@ -897,6 +905,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Attn
   const int pair = p.p_last0 + lp;
   const int tok = pair * p.pair_tokens + x * T + r % T;
   if (tok >= p.n) return;
+  if (p.last_only && tok < p.n - p.last) return;  // final-layer mode: last rows only
   const int head = kvh * p.group + r / T;
   const int r1 = min((pair + 1) * p.pair_tokens, p.n) - 1;
   const int nch = (r1 + 1 + p.chunk_keys - 1) / p.chunk_keys;
@@ -920,11 +929,13 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Attn
     for (int e = 0; e < E; ++e) acc[e] += w * src[lane + 32 * e];
   }
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  const int orow = tok - p.o_row0;
   __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(p.o) + (int64_t)head * p.o_sh +
-                       (int64_t)tok * p.o_st;
+                       (int64_t)orow * p.o_st;
 #pragma unroll
   for (int e = 0; e < E; ++e) dst[lane + 32 * e] = __float2bfloat16_rn(acc[e] * inv);
-  if (lane == 0 && p.lse) p.lse[(int64_t)head * p.n + tok] = wsum > 0.f ? mx + __logf(wsum) : -INFINITY;
+  if (lane == 0 && p.lse)
+    p.lse[(int64_t)head * (p.n - p.o_row0) + orow] = wsum > 0.f ? mx + __logf(wsum) : -INFINITY;
 }
 
 }  // namespace

@@ -46,11 +46,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   // debug builds: report and trap on a wait that never completes (pipeline deadlock)
   uint64_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins == (1ull << 22)) {
+    ++spins;
+    if (spins == (1ull << 22) && (threadIdx.x & 31) == 0)  // report every stuck warp first
       printf("[watchdog] block %d thread %d stuck on mbarrier smem+%u parity %u\n", blockIdx.x,
              threadIdx.x, smem_u32(bar) & 0xffff, parity);
-      asm volatile("trap;");
-    }
+    if (spins == (1ull << 24)) asm volatile("trap;");
   }
 #else
   while (!mbar_try_wait(bar, parity)) {

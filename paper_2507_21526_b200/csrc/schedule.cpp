@@ -12,7 +12,7 @@ namespace ta {
 static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 bool make_geometry(int64_t n, int hq, int hkv, int d, bool dense, int si, int sl, int last,
-                   Geometry *g, std::string *err) {
+                   Geometry *g, std::string *err, bool last_only) {
   if (n < 1 || hq < 1 || hkv < 1 || hq % hkv != 0) {
     if (err) *err = "bad shape";
     return false;
@@ -30,9 +30,12 @@ bool make_geometry(int64_t n, int hq, int hkv, int d, bool dense, int si, int sl
   r.tile_tokens = kTileRows / r.group;
   r.pair_tokens = kTilesPerItem * r.tile_tokens;
   r.dense = dense;
-  r.si = dense ? 0 : si;
-  r.sl = dense ? 1 : sl;
-  r.last = dense ? 1 : last;
+  r.last_only = !dense && last_only;
+  // Final-layer mode: the rows < N - last that share a pair with last rows are computed
+  // with sink 0 / window 1 and never written.
+  r.si = (dense || r.last_only) ? 0 : si;
+  r.sl = (dense || r.last_only) ? 1 : sl;
+  r.last = dense ? 1 : (r.last_only ? (int)std::min<int64_t>(last, n) : last);
   r.num_pairs = (n + r.pair_tokens - 1) / r.pair_tokens;
   if (dense) {
     r.p_last0 = r.num_pairs;
@@ -40,8 +43,8 @@ bool make_geometry(int64_t n, int hq, int hkv, int d, bool dense, int si, int sl
   } else {
     // Rows >= N - last are "last rows" (reading R1); a pair holding any of them is
     // computed by the split-K pass over all of its causal keys (Algorithm 1).
-    int64_t last_start = std::max<int64_t>(0, n - last);
-    r.p_last0 = last_start / r.pair_tokens;
+    // last = 0 (StreamingMix, reading R12) has no last rows.
+    r.p_last0 = r.last == 0 ? r.num_pairs : std::max<int64_t>(0, n - r.last) / r.pair_tokens;
     r.n_last_pairs = r.num_pairs - r.p_last0;
   }
   *g = r;
@@ -108,7 +111,8 @@ void plan_chunks(Geometry *g, int num_ctas) {
     return;
   }
   int64_t ctot = 0;
-  for (int64_t p = 0; p < g->p_last0; ++p) ctot += item_cost(*g, stream_item(*g, 0, p));
+  if (!g->last_only)
+    for (int64_t p = 0; p < g->p_last0; ++p) ctot += item_cost(*g, stream_item(*g, 0, p));
   for (int64_t p = g->p_last0; p < g->num_pairs; ++p) {
     int64_t r0, r1;
     pair_rows(*g, p, &r0, &r1);
@@ -139,8 +143,9 @@ Schedule build_schedule(const Geometry &g0, int num_ctas) {
         for (int64_t kb = 0; kb < r1 + 1; kb += g.chunk_keys)
           canon.push_back(make_item(kLastQ, kvh, p, kb, std::min<int64_t>(kb + g.chunk_keys, r1 + 1)));
       }
-    for (int kvh = 0; kvh < g.hkv; ++kvh)
-      for (int64_t p = 0; p < g.p_last0; ++p) canon.push_back(stream_item(g, kvh, p));
+    if (!g.last_only)
+      for (int kvh = 0; kvh < g.hkv; ++kvh)
+        for (int64_t p = 0; p < g.p_last0; ++p) canon.push_back(stream_item(g, kvh, p));
   } else {
     for (int kvh = 0; kvh < g.hkv; ++kvh)
       for (int64_t p = 0; p < g.num_pairs; ++p) {
@@ -182,7 +187,7 @@ std::vector<uint8_t> serialize(const Schedule &s) {
   const Geometry &g = s.g;
   uint32_t hdr[16] = {kScheduleMagic,
                       kScheduleVersion,
-                      (uint32_t)(g.dense ? 1 : 0),
+                      (uint32_t)(g.dense ? 1 : (g.last_only ? 2 : 0)),
                       (uint32_t)g.n,
                       (uint32_t)g.hq,
                       (uint32_t)g.hkv,

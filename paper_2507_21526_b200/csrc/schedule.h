@@ -46,9 +46,10 @@ struct Geometry {
   int tile_tokens = 0;  // T = floor(128 / G) tokens per packed Q tile
   int pair_tokens = 0;  // P = kTilesPerItem * T tokens per item
   bool dense = false;
+  bool last_only = false;  // final-layer mode: only the last `last` rows, all causal keys
   int si = 0, sl = 1, last = 1;
   int64_t num_pairs = 0;     // ceil(N / P)
-  int64_t p_last0 = 0;       // first pair containing a row >= N - last (triangle)
+  int64_t p_last0 = 0;       // first pair containing a row >= N - last (num_pairs if none)
   int64_t n_last_pairs = 0;  // num_pairs - p_last0 (triangle), 0 for dense
   int chunk_keys = 0;        // split-K chunk length for LASTQ items
   int s_max = 0;             // max chunks per last pair = ceil(N / chunk_keys)
@@ -63,8 +64,9 @@ struct Schedule {
 
 // Fills the geometry fields that do not depend on num_ctas. Returns false on bad input.
 // chunk_keys / s_max are set by plan_chunks() (they depend on num_ctas).
+// last_only: final-layer mode, only LASTQ items over the last `last` rows (si, sl unused).
 bool make_geometry(int64_t n, int hq, int hkv, int d, bool dense, int si, int sl, int last,
-                   Geometry *g, std::string *err);
+                   Geometry *g, std::string *err, bool last_only = false);
 // Row range [r0, r1] (tokens) of pair p, clipped to N.
 void pair_rows(const Geometry &g, int64_t p, int64_t *r0, int64_t *r1);
 // Sum of 16-rounded block widths over the item's key blocks + kItemOverhead.

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert ta.abi_version() == 1
+    assert ta.abi_version() == 2
 
 
 def test_status_strings():
@@ -40,7 +40,8 @@ def test_status_strings():
 
 @pytest.mark.parametrize("n,si,sl,last", [(512, 4, 64, 64), (32768, 8, 512, 128),
                                           (131072, 8, 512, 128), (1, 8, 512, 128),
-                                          (100, 0, 1, 1), (777, 30, 5, 1000)])
+                                          (100, 0, 1, 1), (777, 30, 5, 1000),
+                                          (4096, 8, 512, 0)])
 def test_pair_count_matches_oracle(n, si, sl, last):
     assert ta.pair_count(n, si, sl, last) == counts.triangle_pairs(n, si, sl, last)
     assert ta.pair_count(n, dense=True) == counts.dense_pairs(n)
@@ -64,8 +65,10 @@ def test_pair_count_errors():
         ta.pair_count(10, -1, 5, 128)
     assert e.value.status == 4
     with pytest.raises(ta.TriattnError) as e:
-        ta.pair_count(10, 1, 5, 0)
+        ta.pair_count(10, 1, 5, -1)
     assert e.value.status == 4
+    # last_q = 0 (StreamingMix) is valid: the streaming count alone
+    assert ta.pair_count(100, 4, 10, 0) == counts.streaming_pairs(100, 4, 10)
 
 
 def test_schedule_export_errors():
@@ -81,6 +84,18 @@ def test_schedule_export_errors():
     with pytest.raises(ta.TriattnError) as e:
         ta.schedule_export(100, 32, 8, 128, 0)
     assert e.value.status == 4
+
+
+def test_last_rows_validation():
+    with pytest.raises(ta.TriattnError) as e:
+        ta.last_rows_schedule_export(100, 32, 8, 128, 148, 0)
+    assert e.value.status == 4
+    assert ta.last_rows_workspace_size(100, 32, 8, 128, 0) == 0
+    assert ta.last_rows_workspace_size(131072, 32, 8, 128, 128) > 0
+    lib = ta._load()
+    p = ta._shape_problem(64, 32, 8, 128)
+    assert lib.last_rows_attn_prefill(ctypes.byref(p), 0, None, 0, None) == 4
+    assert lib.last_rows_attn_prefill(ctypes.byref(p), 16, None, 0, None) == 1  # NULL data
 
 
 def test_workspace_size():

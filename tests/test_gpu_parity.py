@@ -102,6 +102,48 @@ def test_odd_params():
     _full_parity(4, 2, 1200, 128, 3, 2000, 5, False, seed=10)  # window >= N
 
 
+# ---------------------------------------------------------------- NEXT rows f3 / f1
+@pytest.mark.parametrize("hq,hkv,n,si,sl", [(32, 8, 4097, 8, 512), (28, 4, 1000, 64, 128),
+                                            (4, 4, 700, 0, 64)])
+def test_streamingmix_last_zero(hq, hkv, n, si, sl):
+    """last_q = 0: sink + window only, no Last Q-K section (StreamingMix; R12)."""
+    _full_parity(hq, hkv, n, 128, si, sl, 0, False, seed=n + 3, lse=True)
+
+
+def _last_rows_parity(hq, hkv, n, d, r, seed, dist="iid"):
+    q, k, v = synth.make_qkv(hq, hkv, n, d, seed, dist)
+    dev = torch.device("cuda")
+    qd, kd, vd = q.to(dev), k.to(dev), v.to(dev)
+    rr = min(r, n)
+    lse = torch.full((hq, rr), float("nan"), device=dev)
+    o = ta.last_rows_attn_prefill(qd, kd, vd, last_q=r, lse=lse)
+    torch.cuda.synchronize()
+    assert tuple(o.shape) == (hq, rr, d)
+    rows = np.arange(n - rr, n)
+    o_ref, lse_ref, _ = cref.attention(q, k, v, 0, 1, 1, True, rows=rows)   # dense causal rows
+    _compare(o.float().cpu(), o_ref, f"last rows hq{hq} n{n} r{r}")
+    assert np.abs(lse.cpu().double().numpy() - lse_ref).max() < 2e-3
+
+
+@pytest.mark.parametrize("hq,hkv,n,d,r", [(32, 8, 4097, 128, 128), (28, 4, 3001, 128, 100),
+                                          (8, 2, 300, 64, 1000), (8, 8, 1, 128, 16)])
+def test_final_layer_last_rows(hq, hkv, n, d, r):
+    """Final-layer last-row-only attention: the last r rows, all causal keys."""
+    _last_rows_parity(hq, hkv, n, d, r, seed=n + 4)
+
+
+def test_final_layer_last_rows_full_size():
+    """C3 shape (N = 131072): the rows equal the dense oracle rows."""
+    c = synth.CONFIGS["C3"]
+    q, k, v = synth.config_qkv(c, layer=31)
+    dev = torch.device("cuda")
+    o = ta.last_rows_attn_prefill(q.to(dev), k.to(dev), v.to(dev), last_q=c.last)
+    torch.cuda.synchronize()
+    rows = np.arange(c.n - 16, c.n)   # the oracle evaluates a sample of the last rows
+    o_ref, _, _ = cref.attention(q, k, v, 0, 1, 1, True, rows=rows)
+    _compare(o[:, -16:].float().cpu(), o_ref, "C3 last rows")
+
+
 # ---------------------------------------------------------------- structural pins
 def test_v_ones_gives_ones():
     q, k, v = synth.make_qkv(32, 8, 3000, 128, seed=11, dist="ones_v")

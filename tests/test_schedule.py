@@ -22,6 +22,9 @@ CASES = [
     (32768, 32, 8, 128, 8, 512, 128, False, 148),
     (32768, 32, 8, 128, 8, 512, 128, True, 148),
     (32768, 4, 1, 128, 8, 512, 128, False, 148),   # one kv-head shard (8 GPUs)
+    (1000, 32, 8, 128, 8, 512, 0, False, 148),     # StreamingMix: no last rows (reading R12)
+    (4097, 28, 4, 128, 64, 128, 0, False, 148),    # StreamingMix, probe-style sink/window
+    (777, 7, 7, 64, 64, 128, 64, False, 11),       # unfused 64-key sink
 ]
 
 
@@ -65,7 +68,7 @@ def test_items_cover_mask_exactly_once(seed):
     n = rng.randint(1, 1500)
     hkv = 1
     hq = rng.choice([1, 2, 4, 7, 8])
-    si, sl, last = rng.randint(0, 40), rng.randint(1, 300), rng.randint(1, 300)
+    si, sl, last = rng.randint(0, 40), rng.randint(1, 300), rng.randint(0, 300)
     dense = rng.random() < 0.25
     nc = rng.choice([1, 5, 148])
     geo, ck, s_max, per, _ = schedule_ref.schedule(n, hq, hkv, 64, si, sl, last, dense, nc)
@@ -97,3 +100,54 @@ def test_last_rows_go_through_split_k():
         assert i // geo["P"] in last_pairs
     hdr, off, items = schedule_ref.parse(ta.schedule_export(32768, 32, 8, 128, 148))
     assert hdr[0] == schedule_ref.MAGIC and hdr[12] == ck and hdr[15] == s_max
+
+
+LAST_ROWS_CASES = [
+    # n, hq, hkv, d, last, num_ctas
+    (32768, 32, 8, 128, 128, 148),
+    (131072, 32, 8, 128, 128, 148),
+    (4097, 28, 4, 128, 100, 148),
+    (300, 4, 1, 64, 1000, 7),   # last >= N: every row
+    (1, 8, 8, 128, 128, 148),
+]
+
+
+@pytest.mark.parametrize("case", LAST_ROWS_CASES)
+def test_last_rows_export_bytes_equal_independent_enumerator(case):
+    """Final-layer mode: only LASTQ items of the last pairs, kind field 2."""
+    n, hq, hkv, d, last, nc = case
+    got = ta.last_rows_schedule_export(n, hq, hkv, d, nc, last)
+    want = schedule_ref.serialize(n, hq, hkv, d, 8, 512, last, False, nc, last_rows=True)
+    assert got == want
+    hdr, off, items = schedule_ref.parse(got)
+    assert hdr[2] == 2 and all(it[0] == schedule_ref.LASTQ for it in items)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_last_rows_items_cover_last_rows_exactly_once(seed):
+    """Every causal key of every row >= N - r is computed exactly once by the LASTQ chunks."""
+    rng = random.Random(100 + seed)
+    n = rng.randint(1, 1500)
+    hq = rng.choice([1, 2, 4, 7, 8])
+    last = rng.randint(1, 400)
+    nc = rng.choice([1, 5, 148])
+    geo, ck, s_max, per, _ = schedule_ref.schedule(n, hq, 1, 64, 8, 512, last, False, nc, last_rows=True)
+    hits = np.zeros((n, n), dtype=np.int32)
+    for lst in per:
+        for it in lst:
+            assert it[0] == schedule_ref.LASTQ
+            r0, r1 = schedule_ref.rows(geo, it[2])
+            for blk in schedule_ref.item_blocks(geo, it):
+                for i in range(max(r0, n - geo["last"]), r1 + 1):
+                    for j in _block_keeps(geo, it, blk, i):
+                        hits[i, j] += 1
+    want = np.tril(np.ones((n, n), dtype=np.int32))
+    want[: n - geo["last"]] = 0
+    assert np.array_equal(hits, want)
+
+
+def test_streamingmix_has_no_split_k():
+    """last = 0: no LASTQ items and no workspace (StreamingMix deep layer)."""
+    hdr, off, items = schedule_ref.parse(ta.schedule_export(4096, 32, 8, 128, 148, 8, 512, 0))
+    assert items and all(it[0] == schedule_ref.STREAM for it in items)
+    assert ta.workspace_size(4096, 32, 8, 128, 8, 512, 0) == 0
