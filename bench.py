@@ -350,6 +350,55 @@ def main():
             sweep.append(res)
             del q2, k2, v2, o2
 
+    # ---- NEXT rows on 1 GPU (extra keys): final-layer last rows (f1), StreamingMix (f3),
+    # and the C5 attention stack per rank of an 8-way kv-head shard (16 dense + 16 triangle).
+    extras = None
+    if args.sweep and world == 1:
+        extras = {}
+
+        def dev_ms(fn, reps):
+            for _ in range(2):
+                fn()
+            evs = []
+            barrier()
+            for _ in range(reps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                evs.append((a, b))
+            barrier()
+            return sum(a.elapsed_time(b) for a, b in evs) / reps
+
+        r = c.last
+        o_last = torch.empty((c.hq, r, c.d), dtype=torch.bfloat16, device=dev)
+        ms = dev_ms(lambda: ta.last_rows_attn_prefill(qd, kd, vd, o_last, last_q=r), 10)
+        fl = 4 * c.d * c.hq * sum(range(c.n - r + 1, c.n + 1))
+        extras["final_layer_last_rows"] = {
+            "what": f"{c.name}: last {r} rows over all causal keys (P:L245-247)", "ms": ms,
+            "kept_tflops": fl / (ms * 1e-3) / 1e12}
+        ms = dev_ms(lambda: ta.triangle_attn_prefill(qd, kd, vd, od, sink=c.si, window=c.sl, last_q=0), 10)
+        fl = 4 * c.d * c.hq * ta.pair_count(c.n, c.si, c.sl, 0)
+        extras["streamingmix_layer"] = {"what": f"{c.name}: sink {c.si} + window {c.sl}, last 0",
+                                        "ms": ms, "kept_tflops": fl / (ms * 1e-3) / 1e12}
+        stack = []
+        g8 = c.hq // c.hkv
+        for n in (32768, 65536, 131072):
+            q1, k1, v1 = (t.to(dev) for t in synth.make_qkv(g8, 1, n, c.d, seed=n))
+            o1 = torch.empty_like(q1)
+            tri = dev_ms(lambda: ta.triangle_attn_prefill(q1, k1, v1, o1, sink=c.si, window=c.sl,
+                                                          last_q=c.last), 5)
+            den = dev_ms(lambda: ta.dense_attn_prefill(q1, k1, v1, o1), 2)
+            stack.append({"seq_len": n, "triangle_ms": tri, "dense_ms": den,
+                          "stack_ms_16d_16t": 16 * den + 16 * tri, "stack_ms_32d": 32 * den,
+                          "attention_speedup": (32 * den) / (16 * den + 16 * tri)})
+            del q1, k1, v1, o1
+        extras["c5_stack_per_rank_of_8"] = {
+            "what": "per-rank attention kernels of the 32-layer Llama stack (16 dense + 16 triangle, "
+                    "tri_start=16) at an 8-way kv-head shard (1 kv head, 4 q heads per rank); "
+                    "all-gather not included; 1 GPU measures one rank", "points": stack}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_run(c, q, k, v, args.cpu_seconds)
@@ -388,6 +437,8 @@ def main():
         }
         if sweep is not None:
             line["sweep"] = sweep
+        if extras is not None:
+            line["next_rows"] = extras
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

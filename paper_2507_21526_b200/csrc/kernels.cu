@@ -101,6 +101,9 @@ constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
 // instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
+#ifndef TA_TILE_TRIM
+#define TA_TILE_TRIM 0
+#endif
 #ifndef TA_POLY_DEG
 #define TA_POLY_DEG 3
 #endif
@@ -108,6 +111,12 @@ constexpr int kEmpty = 1 << 30;            // canonical empty column interval [k
 #define TA_POLY_MASK 0x25
 #endif
 constexpr int kPolyPairs = TA_POLY_MASK;
+// MMA issuer barrier waits: suspending try_wait (default) or a test_wait spin
+#if defined(TA_MMA_SPIN) && !defined(TA_WATCHDOG)
+#define MMA_WAIT(bar, ph) ptx::mbar_wait_spin(bar, ph)
+#else
+#define MMA_WAIT(bar, ph) ptx::mbar_wait(bar, ph)
+#endif
 #ifndef TA_PINGPONG
 #define TA_PINGPONG 0
 #endif
@@ -181,6 +190,19 @@ __device__ __forceinline__ Blk block_info(const ItemInfo &f, int j) {
   }
   b.ncols = b.sink + round16(b.nk);
   return b;
+}
+
+// S columns Q tile x needs in block b: every kept key satisfies j <= i, and the largest
+// token of tile x is r0 + (x+1) T - 1, so the tail of a block beyond it is masked for the
+// whole tile and its QK^T / softmax / PV are skipped (>= 16 columns, <= b.ncols).
+__device__ __forceinline__ int tile_ncols(const ItemInfo &f, const Blk &b, int x, int T) {
+#if TA_TILE_TRIM
+  const int rmax = f.r0 + (x + 1) * T - 1;
+  const int nk = max(1, min(b.nk, rmax - b.kb + 1));
+  return b.sink + round16(nk);
+#else
+  return b.ncols;
+#endif
 }
 
 __device__ __forceinline__ void ring_pos(uint32_t seq, int stages, uint32_t &slot, uint32_t &ph) {
@@ -451,11 +473,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       const uint64_t dkv = ptx::sdesc_sw128(kvbase, 16, 1024);
       const uint64_t dkv_mn = ptx::sdesc_sw128(kvbase, C::kSlotHalfBytes, 1024);
       // S_x[:, 0:ncols] = Q_x K_slot^T  (K-major A and B, 8 x K=16 steps over d)
-      auto issue_qk = [&](int x, uint32_t kslot, const Blk &b) {
+      auto issue_qk = [&](int x, uint32_t kslot, const ItemInfo &fq, const Blk &b) {
         if (!leader) return;
         const uint64_t a0 = dq + (uint64_t)((x * C::kQTileBytes) >> 4);
         const uint64_t b0 = dkv + (uint64_t)((kslot * C::kSlotBytes) >> 4);
-        const uint32_t idesc = ptx::idesc_bf16(128, b.ncols, 0);
+        const uint32_t idesc = ptx::idesc_bf16(128, tile_ncols(fq, b, x, p.tile_tokens), 0);
 #pragma unroll
         for (int s = 0; s < D / 16; ++s) {
           const uint32_t qo = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
@@ -465,10 +487,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       };
       // O_x += P_x V_slot; P_x (bf16) lives in the S_x columns; V MN-major (d contiguous).
       // k-steps [s0, s0 + 4) of the block (keys 16 s .. 16 s + 15)
-      auto issue_pv = [&](int x, uint32_t vslot, const Blk &b, bool acc, int s0) {
+      auto issue_pv = [&](int x, uint32_t vslot, const ItemInfo &fq, const Blk &b, bool acc, int s0) {
         if (!leader) return;
         const uint64_t b0 = dkv_mn + (uint64_t)((vslot * C::kSlotBytes) >> 4);
-        const int ksteps = b.ncols / 16;
+        const int ksteps = tile_ncols(fq, b, x, p.tile_tokens) / 16;
         const uint32_t pcol = tmem + 128u * x;
         // P of keys [64h, 64h + 64) sits in TMEM columns [64h, 64h + 32) of S_x when two
         // threads share a row (each writes over its own S columns), else in [0, 64).
@@ -490,24 +512,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         item_info(p, p.items[it_beg], f);
         uint32_t ii = it_beg;
         int j = 0;
-        ptx::mbar_wait(q_full, nitem & 1u);
+        MMA_WAIT(q_full, nitem & 1u);
         ptx::tc_fence_after();
         TRACE_MM(16, nitem);
         Blk b = block_info(f, 0);
         uint32_t kslot, kph, vslot, vph;
         ring_pos(seq, C::kStages, kslot, kph);
-        ptx::mbar_wait(&kv_full[kslot], kph);
+        MMA_WAIT(&kv_full[kslot], kph);
         ptx::tc_fence_after();
-        issue_qk(0, kslot, b);
+        issue_qk(0, kslot, f, b);
         commit(&s_full[0]);
-        issue_qk(1, kslot, b);
+        issue_qk(1, kslot, f, b);
         commit(&s_full[1]);
         commit(&kv_empty[kslot]);
         if (f.nb == 1) commit(q_empty);  // Q tiles are free after the item's last QK^T
         while (true) {
           ring_pos(seq + 1, C::kStages, vslot, vph);
           TRACE_MM(9, j);
-          ptx::mbar_wait(&kv_full[vslot], vph);
+          MMA_WAIT(&kv_full[vslot], vph);
           TRACE_MM(17, j);
           // next block in the flat stream (same item j+1, or block 0 of the next item)
           const bool last = (j + 1 == f.nb);
@@ -526,49 +548,49 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           // ---- tile A: PV_A(j), then QK_A(next)
           TRACE_MM(8, j);
-          ptx::mbar_wait(&p_ready[0], pph[0]);
+          MMA_WAIT(&p_ready[0], pph[0]);
           pph[0] ^= 1u;
           ptx::tc_fence_after();
           TRACE_MM(10, j);
           const uint32_t kitem = ii - it_beg;  // item of block j
-          if (j == 0 && kitem > 0) ptx::mbar_wait(&o_free[0], (kitem - 1) & 1u);  // O_A drained
-          issue_pv(0, vslot, b, j > 0, 0);   // keys 0..63 while the softmax finishes 64..127
-          ptx::mbar_wait(&p_hi[0], pph[0] ^ 1u);
+          if (j == 0 && kitem > 0) MMA_WAIT(&o_free[0], (kitem - 1) & 1u);  // O_A drained
+          issue_pv(0, vslot, f, b, j > 0, 0);   // keys 0..63 while the softmax finishes 64..127
+          MMA_WAIT(&p_hi[0], pph[0] ^ 1u);
           ptx::tc_fence_after();
-          issue_pv(0, vslot, b, j > 0, 4);
+          issue_pv(0, vslot, f, b, j > 0, 4);
           TRACE_MM(11, j);
           if (last) commit(&o_full[0]);
           if (more) {
             if (last) {  // the next item's Q tiles
               ++nitem;
-              ptx::mbar_wait(q_full, nitem & 1u);
+              MMA_WAIT(q_full, nitem & 1u);
               TRACE_MM(16, nitem);
             }
             TRACE_MM(18, j);
-            ptx::mbar_wait(&kv_full[kslot1], kph1);
+            MMA_WAIT(&kv_full[kslot1], kph1);
             ptx::tc_fence_after();
             TRACE_MM(19, j);
-            issue_qk(0, kslot1, b1);
+            issue_qk(0, kslot1, f1, b1);
             commit(&s_full[0]);
             TRACE_MM(12, j);
           }
           // ---- tile B: PV_B(j), then QK_B(next)
           TRACE_MM(7, j);
-          ptx::mbar_wait(&p_ready[1], pph[1]);
+          MMA_WAIT(&p_ready[1], pph[1]);
           pph[1] ^= 1u;
           ptx::tc_fence_after();
           TRACE_MM(13, j);
-          if (j == 0 && kitem > 0) ptx::mbar_wait(&o_free[1], (kitem - 1) & 1u);  // O_B drained
-          issue_pv(1, vslot, b, j > 0, 0);
-          ptx::mbar_wait(&p_hi[1], pph[1] ^ 1u);
+          if (j == 0 && kitem > 0) MMA_WAIT(&o_free[1], (kitem - 1) & 1u);  // O_B drained
+          issue_pv(1, vslot, f, b, j > 0, 0);
+          MMA_WAIT(&p_hi[1], pph[1] ^ 1u);
           ptx::tc_fence_after();
-          issue_pv(1, vslot, b, j > 0, 4);
+          issue_pv(1, vslot, f, b, j > 0, 4);
           TRACE_MM(14, j);
           if (last) commit(&o_full[1]);
           commit(&kv_empty[vslot]);
           seq += 2;
           if (!more) break;
-          issue_qk(1, kslot1, b1);
+          issue_qk(1, kslot1, f1, b1);
           commit(&s_full[1]);
           TRACE_MM(15, j);
           commit(&kv_empty[kslot1]);
@@ -664,19 +686,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ptx::tc_fence_after();
         TRACE_SM(20, j);
         uint32_t s[kNCol];
+        // 16-column groups this tile computes (tile_ncols; kHPR == 1): the rest of the S
+        // columns hold no scores of this block and are skipped (they are masked anyway).
+        const int nch = (kHPR == 1 && TA_TILE_TRIM == 1) ? tile_ncols(f, b, x, T) / 16 : kNCol / 16;
         // Two halves: the second TMEM load is in flight while the first half is masked.
 #pragma unroll
         for (int c = 0; c < kNCol / 32; ++c)
-          ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
+          if (c < nch) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int c = kNCol / 32; c < kNCol / 16; ++c)
-          ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
+          if (c < nch) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
         TRACE_SM(24, j);
 #pragma unroll
         for (int c = 0; c < kNCol / 32; ++c) {
           if (c == kNCol / 64) ptx::tmem_wait_ld();
-          if (!warp_full) {
+          if (!warp_full && 2 * c < nch) {
             // kept-column bitmask of chunk c: [a_lo, a_hi] U [b_lo, b_hi] intersected with
             // [32c, 32c + 31]
             const uint32_t m32 = iv_bits(a_lo - 32 * c, a_hi - 32 * c) | iv_bits(b_lo - 32 * c, b_hi - 32 * c);
@@ -689,6 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
         for (int e = 0; e < kNCol; e += 8) {
+          if (e >= 16 * nch) break;
           mx0 = max3(mx0, __uint_as_float(s[e]), __uint_as_float(s[e + 1]));
           mx1 = max3(mx1, __uint_as_float(s[e + 2]), __uint_as_float(s[e + 3]));
           mx2 = max3(mx2, __uint_as_float(s[e + 4]), __uint_as_float(s[e + 5]));
@@ -730,6 +756,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         uint64_t l2a = 0, l2b = 0;  // packed partial row sums (FADD2)
 #pragma unroll
         for (int c = 0; c < kNCol / 16; ++c) {
+          if (c >= nch) {
+            if (kHPR == 1 && c == 3) {  // keep the p_ready hand-off when the block is short
+              ptx::tmem_wait_st();
+              ptx::tc_fence_before();
+              ptx::mbar_arrive(&p_ready[x]);
+            }
+            continue;
+          }
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {

@@ -14,9 +14,10 @@ c = synth.CONFIGS[name]
 q, k, v = (t.cuda() for t in synth.config_qkv(c, 16))
 lib = ta._load()
 lib.ta_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-NAMES = {1: "PR.Q", 2: "PR.K", 3: "PR.V", 16: "MM.gotQ", 18: "MM.waitK", 12: "MM.QK", 9: "MM.waitV", 10: "MM.PVlo",
-         11: "MM.PVhi", 20: "SM.gotS", 21: "SM.end", 24: "SM.ldS", 25: "SM.max", 26: "SM.exp", 27: "SM.waitPf",
-         28: "SM.gotPf", 29: "SM.waitS", 30: "EP.waitA", 31: "EP.waitB", 32: "EP.gotA", 33: "EP.gotB", 34: "EP.doneA", 35: "EP.doneB"}
+NAMES = {1: "PR.Q", 2: "PR.K", 3: "PR.V", 16: "MM.gotQ", 9: "MM.waitV", 17: "MM.gotV", 8: "MM.waitP",
+         10: "MM.gotP", 11: "MM.PV", 18: "MM.waitK", 19: "MM.gotK", 12: "MM.QK", 20: "SM.gotS", 21: "SM.end",
+         24: "SM.ldS", 25: "SM.max", 26: "SM.exp", 27: "SM.waitPf", 28: "SM.gotPf", 29: "SM.waitS",
+         30: "EP.waitA", 31: "EP.waitB", 32: "EP.gotA", 33: "EP.gotB", 34: "EP.doneA", 35: "EP.doneB"}
 for cta in (0,):
     os.environ["TA_TRACE_CTA"] = str(cta)
     for _ in range(2):
