@@ -218,11 +218,11 @@ def main():
 
     from paper_2507_21526_b200 import shard
     c = synth.CONFIGS[args.workload]
-    if c.hkv % world != 0:
-        raise SystemExit(f"kv heads {c.hkv} not divisible by world size {world}")
-    hkv_l = c.hkv // world
-    g = c.hq // c.hkv
-    hq_l = hkv_l * g
+    try:
+        plan = shard.head_plan(c.hq, c.hkv, world)   # kv-head shards, or q-head split (Qwen x8)
+    except ValueError as e:
+        raise SystemExit(str(e))
+    hq_l = plan[rank][3] - plan[rank][2]
     q, k, v = synth.config_qkv(c, layer=16)      # CPU bf16, same recipe as the parity tests
     qs, ks, vs = (t.contiguous() for t in shard.shard_qkv(q, k, v, rank, world))
     qd, kd, vd = qs.to(dev), ks.to(dev), vs.to(dev)
@@ -237,7 +237,7 @@ def main():
         else:
             ta.triangle_attn_prefill(qd, kd, vd, od, sink=c.si, window=c.sl, last_q=c.last)
         if world > 1:
-            shard.gather_heads(od, world, out=o_full)
+            shard.gather_heads(od, world, out=o_full, plan=plan)
 
     def barrier():
         torch.cuda.synchronize()
@@ -416,7 +416,9 @@ def main():
             "config": {"workload": f"{args.workload}: {c.name}, one triangle (deep) layer, "
                                    f"Hq={c.hq} Hkv={c.hkv} d={c.d} si/sl/last={c.si}/{c.sl}/{c.last}",
                        "global_batch": 1, "seq_len": c.n,
-                       "parallelism": f"kv-head shard x{world}" + (" + NCCL all-gather of O" if world > 1 else ""),
+                       "parallelism": (f"kv-head shard x{world}" if world <= c.hkv else
+                                       f"q-head split x{world} ({world // c.hkv} ranks per kv head)")
+                                      + (" + NCCL all-gather of O" if world > 1 else ""),
                        "l2": "flushed (512 MiB write) before every timed step; inputs 1.5 GB > L2"},
             "ms_per_layer": ms_tri,
             "dense_ms_per_layer": dense_ms,

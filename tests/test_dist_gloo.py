@@ -29,14 +29,15 @@ def _worker(rank, world, port, cfg, ret):
     q, k, v = synth.make_qkv(hq, hkv, n, d, seed=77)
     qs, ks, vs = shard.shard_qkv(q, k, v, rank, world)
     o, _, _ = cref.attention(qs.contiguous(), ks.contiguous(), vs.contiguous(), si, sl, last, False)
-    full = shard.gather_heads(torch.from_numpy(o).float(), world)
+    full = shard.gather_heads(torch.from_numpy(o).float(), world, plan=shard.head_plan(hq, hkv, world))
     if rank == 0:
         ret.put(full.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg", [(8, 4, 300, 32, 4, 40, 30), (28, 4, 200, 16, 8, 64, 16)])
+@pytest.mark.parametrize("cfg", [(8, 4, 300, 32, 4, 40, 30), (28, 4, 200, 16, 8, 64, 16),
+                                 (7, 1, 150, 16, 8, 32, 20)])   # Qwen-like group split 3 + 4
 def test_sharded_equals_unsharded(cfg):
     world = 2
     ctx = mp.get_context("spawn")
@@ -74,3 +75,15 @@ def test_schedule_per_shard_is_a_kv_head_slice():
     stream_full = sorted((p, kb, ke) for kind, kvh, p, kb, ke in items_full if kvh == 0 and kind == 0)
     stream_shard = sorted((p, kb, ke) for kind, kvh, p, kb, ke in items_shard if kind == 0)
     assert stream_full == stream_shard
+
+
+def test_head_plan_qwen_on_8():
+    """Qwen2.5-7B (Hq 28, Hkv 4) on 8 ranks: two ranks per kv head, q heads split 3 + 4."""
+    plan = shard.head_plan(28, 4, 8)
+    assert plan[0] == (0, 1, 0, 3) and plan[1] == (0, 1, 3, 7) and plan[7] == (3, 4, 24, 28)
+    covered = sorted(h for (_, _, a, b) in plan for h in range(a, b))
+    assert covered == list(range(28))
+    assert all(q0 // 7 == kv0 and (q1 - 1) // 7 == kv0 for (kv0, _, q0, q1) in plan)
+    assert shard.head_plan(32, 8, 8) == [(r, r + 1, 4 * r, 4 * r + 4) for r in range(8)]
+    with pytest.raises(ValueError):
+        shard.head_plan(28, 4, 6)
