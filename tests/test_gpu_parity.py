@@ -219,3 +219,43 @@ def test_full_size_sampled_rows(name):
     o_ref, lse_ref, _ = cref.attention(q, k, v, c.si, c.sl, c.last, False, rows=rows)
     _compare(o[:, rows], o_ref, name)
     assert np.abs(lse[:, rows].double().numpy() - lse_ref).max() < 2e-3
+
+
+# ---------------------------------------------------------------- f4: synthetic prefill model
+def test_synthetic_prefill_model_matches_cpu_reference():
+    """A 3-layer Llama-shaped stack (layer 0 dense, 1-2 triangle) with the kernels on
+    strided token-major views equals a CPU bf16 reference whose attention is the oracle."""
+    import torch.nn.functional as F
+    from paper_2507_21526_b200 import prefill_model as pm
+    shape = pm.ModelShape("tiny", 512, 8, 2, 64, 1024, 3, 1)
+    dev = torch.device("cuda")
+    m = pm.SyntheticPrefill(shape, dev, seed=3)
+    n, si, sl, last = 700, 4, 64, 64
+    x = (torch.randn(n, shape.hidden, generator=torch.Generator().manual_seed(4)) * 0.5).to(torch.bfloat16)
+    y = m.forward(x.to(dev), sink=si, window=sl, last_q=last).float().cpu()
+    # CPU reference: same ops in bf16, attention from the fp64 oracle
+    cpu = pm.SyntheticPrefill.__new__(pm.SyntheticPrefill)
+    cpu.s, cpu.device, cpu.dtype, cpu._rope = shape, torch.device("cpu"), torch.bfloat16, {}
+    cpu.w_qkv, cpu.w_o, cpu.w_gu, cpu.w_down = (w.cpu() for w in (m.w_qkv, m.w_o, m.w_gu, m.w_down))
+    cos, sin = cpu.rope_tables(n)
+    nq, nkv = shape.hq * shape.d, shape.hkv * shape.d
+    xr = x.clone()
+    for layer in range(shape.layers):
+        h = cpu._rms(xr)
+        qkv = F.linear(h, cpu.w_qkv)
+        q = cpu._rope_apply(qkv[:, :nq].view(n, shape.hq, shape.d), cos, sin)
+        k = cpu._rope_apply(qkv[:, nq:nq + nkv].view(n, shape.hkv, shape.d), cos, sin)
+        v = qkv[:, nq + nkv:].view(n, shape.hkv, shape.d)
+        o, _, _ = cref.attention(q.transpose(0, 1).contiguous(), k.transpose(0, 1).contiguous(),
+                                 v.transpose(0, 1).contiguous(), si, sl, last, layer < shape.tri_start)
+        attn = torch.from_numpy(o).to(torch.bfloat16).transpose(0, 1).reshape(n, nq)
+        xr = xr + F.linear(attn, cpu.w_o)
+        h = cpu._rms(xr)
+        gu = F.linear(h, cpu.w_gu)
+        xr = xr + F.linear(F.silu(gu[:, :shape.inter]) * gu[:, shape.inter:], cpu.w_down)
+    ref = xr[-last:].float()
+    err = (y - ref).abs()
+    assert err.mean().item() <= 2e-2 * ref.abs().mean().item(), (err.mean().item(), ref.abs().mean().item())
+    # the final-layer last-rows mode gives the same last rows
+    y2 = m.forward(x.to(dev), sink=si, window=sl, last_q=last, final_last_rows=True).float().cpu()
+    assert (y2 - y).abs().max().item() <= 0.05 * ref.abs().max().item()
