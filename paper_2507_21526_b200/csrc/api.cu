@@ -316,8 +316,8 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
 #ifdef TA_TRACE
   {
     static unsigned long long *tbuf = nullptr;
-    if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * 65536 * 5);
-    cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 65536 * 5, stream);
+    if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * 65536 * 8);
+    cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 65536 * 8, stream);
     prm.trace = tbuf;
     const char *e = getenv("TA_TRACE_CTA");
     prm.trace_cta = e ? atoi(e) : 0;
@@ -536,7 +536,7 @@ ta_status ta_profile_end(double *attn_ms, int64_t *attn_launches, double *merge_
 /* Debug build only: copy the last launch's timeline (4 x 65536 u64) to the host. */
 ta_status ta_debug_trace_read(void *host, size_t cap) {
   if (!g_trace_buf) return TA_ERR_CUDA;
-  size_t n = sizeof(unsigned long long) * 65536 * 5;
+  size_t n = sizeof(unsigned long long) * 65536 * 8;
   cudaMemcpy(host, g_trace_buf, cap < n ? cap : n, cudaMemcpyDeviceToHost);
   return TA_OK;
 }

@@ -46,11 +46,14 @@ namespace {
 #define TRACE_PR(code, arg) do { if (leader) TRACE_AT(0, trc, code, arg); } while (0)
 #define TRACE_MM(code, arg) do { if (leader) TRACE_AT(65536, trc, code, arg); } while (0)
 #define TRACE_SM(code, arg) do { if (lane == 0 && wq == 0 && hc == 0) TRACE_AT(131072 + 65536 * x, trc, code, arg); } while (0)
+// tile A warps 1-3 (drift across the four warps of a tile): roles 5-7
+#define TRACE_SMW(code, arg) do { if (lane == 0 && x == 0 && wq > 0 && hc == 0) TRACE_AT(65536 * (4 + wq), trc, code, arg); } while (0)
 #define TRACE_EP(code, arg) do { if (lane == 0 && eq == 0 && x0 == 0) TRACE_AT(262144, trc, code, arg); } while (0)
 #else
 #define TRACE_PR(code, arg) do {} while (0)
 #define TRACE_MM(code, arg) do {} while (0)
 #define TRACE_SM(code, arg) do {} while (0)
+#define TRACE_SMW(code, arg) do {} while (0)
 #define TRACE_EP(code, arg) do {} while (0)
 #endif
 
@@ -93,14 +96,20 @@ constexpr int kAllocWarp = kMmaWarp + 2;
 constexpr int kThreads = 32 * (kSoftmaxWarps + kEpiWarps + 4);
 constexpr int kNCol = 128 / kHPR;  // S columns per softmax thread
 // setmaxnreg split of the register file (launch: 65536 / kThreads, rounded down to 8)
-constexpr int kRegSoftmax = kEpiWarps == 4 ? (kHPR == 1 ? 184 : 96) : (kHPR == 1 ? 176 : 88);
-constexpr int kRegEpi = kEpiWarps == 4 ? (kHPR == 1 ? 72 : 48) : 40;
+#ifndef TA_REG_SOFTMAX
+#define TA_REG_SOFTMAX 184
+#endif
+constexpr int kRegSoftmax = kEpiWarps == 4 ? (kHPR == 1 ? TA_REG_SOFTMAX : 96) : (kHPR == 1 ? 176 : 88);
+constexpr int kRegEpi = kEpiWarps == 4 ? (kHPR == 1 ? (2048 - 8 * TA_REG_SOFTMAX) / 8 : 48) : 40;
 constexpr int kRegOther = kEpiWarps == 4 ? kRegEpi : (kHPR == 1 ? 48 : 40);
 constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
 // instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
+#ifndef TA_SM_WAIT
+#define TA_SM_WAIT 0
+#endif
 #ifndef TA_TILE_TRIM
 #define TA_TILE_TRIM 0
 #endif
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       uint32_t seq = 0, nitem = 0;
       const uint32_t q_bytes = 2u * C::kHalves * 128u * p.tile_tokens * p.group;
       auto load_q = [&](const ItemInfo &f, uint32_t nitem) {
-        ptx::mbar_wait(q_empty, (nitem & 1u) ^ 1u);
+        ptx::mbar_wait_lazy(q_empty, (nitem & 1u) ^ 1u);
         if (leader) {
           ptx::mbar_arrive_expect_tx(q_full, q_bytes);
           for (int x = 0; x < 2; ++x)
@@ -414,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         for (int kv = 0; kv < 2; ++kv, ++seq) {
           uint32_t slot, ph;
           ring_pos(seq, C::kStages, slot, ph);
-          ptx::mbar_wait(&kv_empty[slot], ph ^ 1u);
+          ptx::mbar_wait_lazy(&kv_empty[slot], ph ^ 1u);
           if (leader) {
             // one 128-row box, or 16 sink rows + a 112-row band box (fused first block)
             ptx::mbar_arrive_expect_tx(&kv_full[slot], kBlockKeys * 128 * C::kHalves);
@@ -681,10 +690,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                           (a_lo <= 0 && b_lo <= a_hi + 1 && b_hi >= L);
         const bool warp_full = __all_sync(0xffffffffu, full);
 
+#if TA_SM_WAIT == 1
+        while (!ptx::mbar_try_wait_hint(&s_full[x], sph, 1000000u)) {
+        }
+#else
         ptx::mbar_wait(&s_full[x], sph);
+#endif
         sph ^= 1u;
         ptx::tc_fence_after();
         TRACE_SM(20, j);
+        TRACE_SMW(20, j);
         uint32_t s[kNCol];
         // 16-column groups this tile computes (tile_ncols; kHPR == 1): the rest of the S
         // columns hold no scores of this block and are skipped (they are masked anyway).
@@ -806,6 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ptx::tc_fence_before();
         ptx::mbar_arrive((kHPR == 2 && hc == 0) ? &p_ready[x] : &p_hi[x]);
         TRACE_SM(21, j);
+        TRACE_SMW(21, j);
       }
       // ---------------- hand the item's row statistics to the epilogue warpgroup
       {
@@ -845,8 +861,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const int tok = f.r0 + x * T + toff;
         const bool valid = row_in_tile && tok < p.n;
         TRACE_EP(30 + x, kitem);
-        ptx::mbar_wait(&l_ready[x], par);
-        ptx::mbar_wait(&o_full[x], par);
+        ptx::mbar_wait_lazy(&l_ready[x], par);
+        ptx::mbar_wait_lazy(&o_full[x], par);
         ptx::tc_fence_after();
         TRACE_EP(32 + x, kitem);
         const float l_row = lds_f32(ptx::smem_u32(red_l + ((par * 2 + x) * 2 + 0) * kTileRows + r)) +

@@ -3,6 +3,9 @@
 // commit, ld, st, fences) and the UMMA shared-memory / instruction descriptors.
 // Compile with -gencode arch=compute_100a,code=sm_100a.
 #pragma once
+#ifndef TA_LAZY_WAIT
+#define TA_LAZY_WAIT 0
+#endif
 #include <cstdint>
 #include <cstdio>
 
@@ -74,6 +77,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 #endif
 }
 
+// try_wait with an explicit suspend-time hint (ns): the warp sleeps until the phase
+// completes or the hint expires instead of re-issuing the poll loop.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+// Waits for latency-tolerant roles (epilogue, producer): long suspend hint, or a
+// nanosleep back-off between polls.
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t *bar, uint32_t parity) {
+#if defined(TA_WATCHDOG)
+  mbar_wait(bar, parity);
+#elif TA_LAZY_WAIT == 1
+  while (!mbar_try_wait_hint(bar, parity, 1000000u)) {
+  }
+#elif TA_LAZY_WAIT == 2
+  while (!mbar_try_wait(bar, parity)) __nanosleep(128);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 // One lane of a converged warp (the same lane every call) returns true.
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;

@@ -17,3 +17,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn
   -o gpurun_out/prof_attn_${TAG} -f \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-dense --no-e2e > gpurun_out/ncu_full_${TAG}.log 2>&1; echo "ncu full rc=$?"
 CASE=3 timeout 600 compute-sanitizer --tool memcheck --leak-check no python scripts/debug_small.py > gpurun_out/memcheck_${TAG}.log 2>&1; echo "memcheck rc=$? $(grep -E 'ERROR SUMMARY' gpurun_out/memcheck_${TAG}.log | tail -1)"
+timeout 900 python scripts/ttft_synth.py > gpurun_out/ttft_${TAG}.json 2> gpurun_out/ttft_${TAG}.err; echo "ttft rc=$?"

@@ -26,10 +26,10 @@ for cta in (0,):
         else:
             ta.triangle_attn_prefill(q, k, v, sink=c.si, window=c.sl, last_q=c.last)
     torch.cuda.synchronize()
-    buf = np.zeros(5 * 65536, dtype=np.uint64)
+    buf = np.zeros(8 * 65536, dtype=np.uint64)
     lib.ta_debug_trace_read(buf.ctypes.data, buf.nbytes)
     ev = []
-    for role in range(5):
+    for role in range(8):
         seg = buf[role * 65536:(role + 1) * 65536]
         seg = seg[seg != 0]
         for w in seg:
@@ -86,3 +86,13 @@ for cta in (0,):
         n = min(len(ga), len(da)); m = min(len(gb), len(db))
         print("epilogue tile work (median cycles): A", np.median(np.array(da[:n]) - np.array(ga[:n])),
               "B", np.median(np.array(db[:m]) - np.array(gb[:m])))
+
+# drift across the four warps of tile A: per block, spread of "end" (and gotS) times
+for code, nm in ((20, "gotS"), (21, "end")):
+    per = [[t for t, r, cd, a in ev if r == rr and cd == code] for rr in (2, 5, 6, 7)]
+    m = min(len(x) for x in per)
+    if m:
+        arr = np.array([x[:m] for x in per], dtype=np.float64)
+        spread = arr.max(0) - arr.min(0)
+        slow = np.bincount(arr.argmax(0), minlength=4)
+        print(f"tile A warps {nm}: spread med {np.median(spread):.0f} mean {spread.mean():.0f}; slowest warp counts {slow.tolist()}")
