@@ -128,3 +128,12 @@ def test_no_cpu_fallback_in_product():
             assert not re.search(r"^\s*(from|import)\s+oracle", s, flags=re.M), f
             for bad in ("scaled_dot_product_attention", ".softmax(", "torch.exp(", "np.exp("):
                 assert bad not in s, (f, bad)
+
+
+def test_graft_entry_build():
+    """The driver's build() check: compiles (or finds current) libraries and checks the ABI."""
+    import importlib
+    import sys
+    sys.path.insert(0, ROOT)
+    g = importlib.import_module("__graft_entry__")
+    g.build()
