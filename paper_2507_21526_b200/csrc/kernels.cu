@@ -107,6 +107,9 @@ constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
 // instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
+#ifndef TA_SUM_ROUNDED
+#define TA_SUM_ROUNDED 0
+#endif
 #ifndef TA_SM_WAIT
 #define TA_SM_WAIT 0
 #endif
@@ -793,11 +796,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
               p0 = ptx::ex2(x0);            // MUFU
               p1 = ptx::ex2(x1);
             }
-            if (e & 2)
-              l2b = fadd2(l2b, f2pack(p0, p1));
-            else
-              l2a = fadd2(l2a, f2pack(p0, p1));
             pk[e / 2] = ptx::pack_bf16(p0, p1);
+#if TA_SUM_ROUNDED
+            // row sum of the bf16-rounded P the PV MMA actually uses (exact normalisation)
+            const uint64_t pr = u2pack(pk[e / 2] << 16, pk[e / 2] & 0xffff0000u);
+#else
+            const uint64_t pr = f2pack(p0, p1);
+#endif
+            if (e & 2)
+              l2b = fadd2(l2b, pr);
+            else
+              l2a = fadd2(l2a, pr);
           }
           ptx::tmem_st8(tS + c * 8, pk);
           if (kHPR == 1 && c == 3) {
