@@ -210,7 +210,7 @@ def _sample_rows(n, last, rng):
     return np.array(sorted(r for r in rows if 0 <= r < n))
 
 
-@pytest.mark.parametrize("name", ["C2"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4b"])
 def test_full_size_sampled_rows(name):
     c = synth.CONFIGS[name]
     q, k, v = synth.config_qkv(c, layer=16)
