@@ -97,11 +97,20 @@ constexpr int kThreads = 32 * (kSoftmaxWarps + kEpiWarps + 4);
 constexpr int kNCol = 128 / kHPR;  // S columns per softmax thread
 // setmaxnreg split of the register file (launch: 65536 / kThreads, rounded down to 8)
 #ifndef TA_REG_SOFTMAX
-#define TA_REG_SOFTMAX 184
+#define TA_REG_SOFTMAX 176
 #endif
 constexpr int kRegSoftmax = kEpiWarps == 4 ? (kHPR == 1 ? TA_REG_SOFTMAX : 96) : (kHPR == 1 ? 176 : 88);
-constexpr int kRegEpi = kEpiWarps == 4 ? (kHPR == 1 ? (2048 - 8 * TA_REG_SOFTMAX) / 8 : 48) : 40;
-constexpr int kRegOther = kEpiWarps == 4 ? kRegEpi : (kHPR == 1 ? 48 : 40);
+#ifndef TA_REG_EPI  // epilogue warpgroup; the issuer warpgroup gets the rest (2 S + E + O = 512)
+#define TA_REG_EPI ((2048 - 8 * TA_REG_SOFTMAX) / 8)
+#endif
+constexpr int kRegEpi = kEpiWarps == 4 ? (kHPR == 1 ? TA_REG_EPI : 48) : 40;
+constexpr int kRegOther = kEpiWarps == 4 ? (kHPR == 1 ? 512 - 2 * TA_REG_SOFTMAX - TA_REG_EPI : 48)
+                                         : (kHPR == 1 ? 48 : 40);
+static_assert(kRegOther >= 24 && kRegOther % 8 == 0 && kRegEpi % 8 == 0, "setmaxnreg split");
+#ifndef TA_WARP_ARRIVE
+#define TA_WARP_ARRIVE 1
+#endif
+constexpr int kArrivePerTile = TA_WARP_ARRIVE ? 4 : kTileRows;  // softmax arrivals per tile
 constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
@@ -128,6 +137,15 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #define MMA_WAIT(bar, ph) ptx::mbar_wait_spin(bar, ph)
 #else
 #define MMA_WAIT(bar, ph) ptx::mbar_wait(bar, ph)
+#endif
+#ifndef TA_TMEM_WIDE
+#define TA_TMEM_WIDE 0
+#endif
+#ifndef TA_EXP_ORDER
+#define TA_EXP_ORDER 1
+#endif
+#ifndef TA_MMA_REMAT
+#define TA_MMA_REMAT 1
 #endif
 #ifndef TA_PINGPONG
 #define TA_PINGPONG 0
@@ -367,11 +385,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     ptx::mbar_init(q_empty, 1);
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&s_full[x], 1);
-      ptx::mbar_init(&p_ready[x], kTileRows);  // first 64 keys of P written
-      ptx::mbar_init(&p_hi[x], kTileRows);     // last 64 keys of P written
+      ptx::mbar_init(&p_ready[x], kArrivePerTile);  // first 64 keys of P written
+      ptx::mbar_init(&p_hi[x], kArrivePerTile);     // last 64 keys of P written
       ptx::mbar_init(&o_full[x], 1);
       ptx::mbar_init(&exp_turn[x], 4 * kHPR);  // one arrival per softmax warp of the other tile
-      ptx::mbar_init(&l_ready[x], kHPR * kTileRows);
+      ptx::mbar_init(&l_ready[x], kHPR * kArrivePerTile);
       ptx::mbar_init(&o_free[x], 4);     // one arrival per epilogue warp
     }
     ptx::fence_mbar_init();
@@ -481,9 +499,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       uint32_t pph[2] = {0, 0};
       // Descriptors are built once; per MMA only the 14-bit start-address field moves
       // (smem offsets < 256 KB, so adding (offset >> 4) to the descriptor never carries).
-      const uint64_t dq = ptx::sdesc_sw128(qbase, 16, 1024);
-      const uint64_t dkv = ptx::sdesc_sw128(kvbase, 16, 1024);
-      const uint64_t dkv_mn = ptx::sdesc_sw128(kvbase, C::kSlotHalfBytes, 1024);
+      uint64_t dq = ptx::sdesc_sw128(qbase, 16, 1024);
+      uint64_t dkv = ptx::sdesc_sw128(kvbase, 16, 1024);
+      uint64_t dkv_mn = ptx::sdesc_sw128(kvbase, C::kSlotHalfBytes, 1024);
+      uint32_t tm = tmem;
+      // Re-materialise the bases every iteration (an opaque asm "redefines" them): the
+      // compiler would otherwise hoist all 32 per-k-step descriptors / TMEM addresses out
+      // of the loop and spill them to local memory in this 72-register warp, putting
+      // local-memory round trips between the waits and the MMA issues.
+      auto opaque_bases = [&]() {
+#if TA_MMA_REMAT
+        asm volatile("" : "+l"(dq), "+l"(dkv), "+l"(dkv_mn), "+r"(tm));
+#endif
+      };
       // S_x[:, 0:ncols] = Q_x K_slot^T  (K-major A and B, 8 x K=16 steps over d)
       auto issue_qk = [&](int x, uint32_t kslot, const ItemInfo &fq, const Blk &b) {
         if (!leader) return;
@@ -494,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         for (int s = 0; s < D / 16; ++s) {
           const uint32_t qo = ((s >> 2) * C::kHalfBytes + (s & 3) * 32) >> 4;
           const uint32_t ko = ((s >> 2) * C::kSlotHalfBytes + (s & 3) * 32) >> 4;
-          ptx::mma_ss(tmem + 128u * x, a0 + qo, b0 + ko, idesc, s > 0 ? 1u : 0u);
+          ptx::mma_ss(tm + 128u * x, a0 + qo, b0 + ko, idesc, s > 0 ? 1u : 0u);
         }
       };
       // O_x += P_x V_slot; P_x (bf16) lives in the S_x columns; V MN-major (d contiguous).
@@ -503,13 +531,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         if (!leader) return;
         const uint64_t b0 = dkv_mn + (uint64_t)((vslot * C::kSlotBytes) >> 4);
         const int ksteps = tile_ncols(fq, b, x, p.tile_tokens) / 16;
-        const uint32_t pcol = tmem + 128u * x;
+        const uint32_t pcol = tm + 128u * x;
         // P of keys [64h, 64h + 64) sits in TMEM columns [64h, 64h + 32) of S_x when two
         // threads share a row (each writes over its own S columns), else in [0, 64).
 #pragma unroll
         for (int s = s0; s < s0 + 4; ++s)
           if (s < ksteps)
-            ptx::mma_ts(tmem + 256u + 128u * x,
+            ptx::mma_ts(tm + 256u + 128u * x,
                         pcol + (s / (8 / kHPR)) * 64 + (s % (8 / kHPR)) * 8,
                         b0 + (uint64_t)(s * (2048 >> 4)), idesc_pv, (acc || s > 0) ? 1u : 0u);
       };
@@ -539,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         commit(&kv_empty[kslot]);
         if (f.nb == 1) commit(q_empty);  // Q tiles are free after the item's last QK^T
         while (true) {
+          opaque_bases();
           ring_pos(seq + 1, C::kStages, vslot, vph);
           TRACE_MM(9, j);
           MMA_WAIT(&kv_full[vslot], vph);
@@ -634,6 +663,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     const uint32_t my_max_s = ptx::smem_u32(red_max + (x * 2 * 2 + hc) * kTileRows + r);
     const uint32_t peer_max_s = ptx::smem_u32(red_max + (x * 2 * 2 + (1 - hc)) * kTileRows + r);
     uint32_t sph = 0, ecount = 0, kitem_sm = 0;
+    // Softmax -> MMA / epilogue hand-offs: one arrival per warp (TA_WARP_ARRIVE; the
+    // warp-collective tcgen05.wait::st / __syncwarp order the other lanes' TMEM and shared
+    // stores before lane 0's release-arrive) instead of 32 serialised same-address arrivals.
+    auto sm_arrive = [&](uint64_t *bar) {
+      if (TA_WARP_ARRIVE) {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar);
+      } else {
+        ptx::mbar_arrive(bar);
+      }
+    };
+    auto sm_arrive_state = [&](uint64_t *bar) -> uint64_t {
+      if (TA_WARP_ARRIVE) {
+        __syncwarp();
+        uint64_t st = 0;
+        if (lane == 0) st = ptx::mbar_arrive_state(bar);
+        return __shfl_sync(0xffffffffu, st, 0);
+      }
+      return ptx::mbar_arrive_state(bar);
+    };
 #ifdef TA_TRACE
     uint32_t trc = 0;
 #endif
@@ -708,13 +757,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         // columns hold no scores of this block and are skipped (they are masked anyway).
         const int nch = (kHPR == 1 && TA_TILE_TRIM == 1) ? tile_ncols(f, b, x, T) / 16 : kNCol / 16;
         // Two halves: the second TMEM load is in flight while the first half is masked.
+        if (TA_TMEM_WIDE && kHPR == 1 && TA_TILE_TRIM == 0) {  // 32-column loads
 #pragma unroll
-        for (int c = 0; c < kNCol / 32; ++c)
-          if (c < nch) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
-        ptx::tmem_wait_ld();
+          for (int c = 0; c < 2; ++c) ptx::tmem_ld32(tS + c * 32, s + c * 32);
+          ptx::tmem_wait_ld();
 #pragma unroll
-        for (int c = kNCol / 32; c < kNCol / 16; ++c)
-          if (c < nch) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
+          for (int c = 2; c < 4; ++c) ptx::tmem_ld32(tS + c * 32, s + c * 32);
+        } else {
+#pragma unroll
+          for (int c = 0; c < kNCol / 32; ++c)
+            if (c < nch) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int c = kNCol / 32; c < kNCol / 16; ++c)
+            if (c < nch) ptx::tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(s + c * 16), 0);
+        }
         TRACE_SM(24, j);
 #pragma unroll
         for (int c = 0; c < kNCol / 32; ++c) {
@@ -770,19 +827,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         // the other tile.
         if (kPingPong) ptx::mbar_wait(&exp_turn[x], (ecount & 1u) ^ (x == 0 ? 1u : 0u));
         const uint64_t sc2 = f2pack(sc, sc);
-        const uint64_t nref2 = f2pack(-ref, -ref);
+        uint64_t nref2 = f2pack(-ref, -ref);
         uint64_t l2a = 0, l2b = 0;  // packed partial row sums (FADD2)
+        uint32_t pkw[16];           // bf16 P pairs of one (TA_TMEM_WIDE: two) 16-key chunks
 #pragma unroll
         for (int c = 0; c < kNCol / 16; ++c) {
           if (c >= nch) {
             if (kHPR == 1 && c == 3) {  // keep the p_ready hand-off when the block is short
               ptx::tmem_wait_st();
               ptx::tc_fence_before();
-              ptx::mbar_arrive(&p_ready[x]);
+              sm_arrive(&p_ready[x]);
             }
             continue;
           }
-          uint32_t pk[8];
+          uint32_t *pk = pkw + (TA_TMEM_WIDE ? (c & 1) * 8 : 0);
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
             const int col = c * 16 + e;
@@ -808,12 +866,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             else
               l2a = fadd2(l2a, pr);
           }
-          ptx::tmem_st8(tS + c * 8, pk);
+          if (!TA_TMEM_WIDE)
+            ptx::tmem_st8(tS + c * 8, pk);
+          else if (c & 1)  // two chunks (32 keys) per 16-column store
+            ptx::tmem_st16(tS + (c - 1) * 8, pkw);
           if (kHPR == 1 && c == 3) {
             // keys 0..63 of P are in TMEM: the MMA can start PV on them right away
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&p_ready[x]);
+#if TA_EXP_ORDER
+            // The exponentials of keys 64..127 take their offset from the arrive's state
+            // token, so ptxas cannot schedule them above the hand-off (it otherwise hoists
+            // all 128 exponentials above the first TMEM store and p_ready fires at the end
+            // of the row, leaving PV nothing to overlap).
+            nref2 = ptx::after_token(nref2, sm_arrive_state(&p_ready[x]));
+#else
+            sm_arrive(&p_ready[x]);
+#endif
           }
         }
         __syncwarp();
@@ -828,7 +897,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive((kHPR == 2 && hc == 0) ? &p_ready[x] : &p_hi[x]);
+        sm_arrive((kHPR == 2 && hc == 0) ? &p_ready[x] : &p_hi[x]);
         TRACE_SM(21, j);
         TRACE_SMW(21, j);
       }
@@ -841,7 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         sts_f32(ptx::smem_u32(red_l + ((par * 2 + x) * 2 + hc) * kTileRows + r), l_run);
         if (kHPR == 1) sts_f32(ptx::smem_u32(red_l + ((par * 2 + x) * 2 + 1) * kTileRows + r), 0.f);
         if (hc == 0) sts_f32(ptx::smem_u32(red_m + (par * 2 + x) * kTileRows + r), m_run);
-        ptx::mbar_arrive(&l_ready[x]);
+        sm_arrive(&l_ready[x]);
         ++kitem_sm;
       }
     }
