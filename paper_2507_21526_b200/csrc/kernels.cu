@@ -85,12 +85,19 @@ struct Cfg {
 #endif
 constexpr int kHPR = TA_HPR;
 constexpr int kSoftmaxWarps = 8 * kHPR;
-constexpr int kEpiWarp0 = kSoftmaxWarps;  // epilogue warps: 4 per Q tile (TA_EPI_WARPS = 8) or
-#ifndef TA_EPI_WARPS                       // 4 serving both tiles in turn (default)
+#ifndef TA_EPI_WARPS  // epilogue warps: 4 per Q tile (TA_EPI_WARPS = 8) or 4 serving both tiles in turn
 #define TA_EPI_WARPS 4
 #endif
 constexpr int kEpiWarps = TA_EPI_WARPS;
-constexpr int kMmaWarp = kEpiWarp0 + kEpiWarps;
+// TA_EPI_LOW: the epilogue warpgroup takes warps 0-3 and the softmax warps 4-11, so the
+// softmax (the critical path) wins issue arbitration over the epilogue on every SMSP.
+#ifndef TA_EPI_LOW
+#define TA_EPI_LOW 1
+#endif
+constexpr bool kEpiLow = TA_EPI_LOW != 0 && kHPR == 1 && kEpiWarps == 4;
+constexpr int kSmWarp0 = kEpiLow ? kEpiWarps : 0;
+constexpr int kEpiWarp0 = kEpiLow ? 0 : kSoftmaxWarps;
+constexpr int kMmaWarp = kSoftmaxWarps + kEpiWarps;
 constexpr int kTmaWarp = kMmaWarp + 1;
 constexpr int kAllocWarp = kMmaWarp + 2;
 constexpr int kThreads = 32 * (kSoftmaxWarps + kEpiWarps + 4);
@@ -108,14 +115,16 @@ constexpr int kRegOther = kEpiWarps == 4 ? (kHPR == 1 ? 512 - 2 * TA_REG_SOFTMAX
                                          : (kHPR == 1 ? 48 : 40);
 static_assert(kRegOther >= 24 && kRegOther % 8 == 0 && kRegEpi % 8 == 0, "setmaxnreg split");
 #ifndef TA_WARP_ARRIVE
-#define TA_WARP_ARRIVE 1
+#define TA_WARP_ARRIVE 0
 #endif
 constexpr int kArrivePerTile = TA_WARP_ARRIVE ? 4 : kTileRows;  // softmax arrivals per tile
 constexpr float kRescaleThreshold = 8.0f;  // lazy rescale: exponent headroom in log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr int kEmpty = 1 << 30;            // canonical empty column interval [kEmpty, kEmpty]
 // Bit k set: column pair k (of the 8 pairs in every 16 columns) uses the FMA-pipe exp2
-// instead of MUFU.EX2; 0x25 = 3/8 of the exponentials (MUFU is 16/clk/SM on B200).
+// instead of MUFU.EX2.  Default 0: every exponential on MUFU -- with the exp phase bound by
+// the FMA pipe (FFMA2 scale, FADD2 row sum, F2FP) the offload measured slower (cycles per
+// item: 0x25 +2.4 %, 0x11 +2.2 %, 0x01 +0.5 % vs 0x00; scripts/variant_cycles.py).
 #ifndef TA_SUM_ROUNDED
 #define TA_SUM_ROUNDED 0
 #endif
@@ -129,7 +138,7 @@ constexpr int kEmpty = 1 << 30;            // canonical empty column interval [k
 #define TA_POLY_DEG 3
 #endif
 #ifndef TA_POLY_MASK
-#define TA_POLY_MASK 0x25
+#define TA_POLY_MASK 0x00
 #endif
 constexpr int kPolyPairs = TA_POLY_MASK;
 // MMA issuer barrier waits: suspending try_wait (default) or a test_wait spin
@@ -147,10 +156,31 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_MMA_REMAT
 #define TA_MMA_REMAT 1
 #endif
+#ifndef TA_EARLY_K
+#define TA_EARLY_K 1
+#endif
 #ifndef TA_PINGPONG
 #define TA_PINGPONG 0
 #endif
 constexpr bool kPingPong = TA_PINGPONG != 0;
+
+// Causal-profiling debug switches: spin N cycles at a point of one role per key block.
+#ifndef TA_DELAY_MMA
+#define TA_DELAY_MMA 0
+#endif
+#ifndef TA_DELAY_SM
+#define TA_DELAY_SM 0
+#endif
+#ifndef TA_DELAY_TMA
+#define TA_DELAY_TMA 0
+#endif
+__device__ __forceinline__ void spin_cycles(int n) {
+  if (n > 0) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < n) {
+    }
+  }
+}
 
 struct ItemInfo {
   int kind, kvh, pair;
@@ -412,7 +442,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 
   // Register split: softmax warpgroups kRegSoftmax, epilogue kRegEpi, issuers kRegOther.
   if (warp >= kMmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegOther) : "memory");
-  else if (warp >= kEpiWarp0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegEpi) : "memory");
+  else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegEpi) : "memory");
 
   if (warp == kTmaWarp) {
     // ===================== TMA producer (whole warp, one elected lane issues) ==========
@@ -440,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
       };
       auto load_kv = [&](const ItemInfo &f, int j) {
+        spin_cycles(TA_DELAY_TMA);
         const Blk b = block_info(f, j);
         for (int kv = 0; kv < 2; ++kv, ++seq) {
           uint32_t slot, ph;
@@ -586,9 +618,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           if (more) {
             b1 = block_info(f1, j1);
             ring_pos(seq + 2, C::kStages, kslot1, kph1);
+            // K of the next block is normally resident long before it is needed: wait for
+            // it here, off the PV -> QK^T hand-off of tile A.
+            if (TA_EARLY_K) MMA_WAIT(&kv_full[kslot1], kph1);
           }
           // ---- tile A: PV_A(j), then QK_A(next)
           TRACE_MM(8, j);
+          spin_cycles(TA_DELAY_MMA);
           MMA_WAIT(&p_ready[0], pph[0]);
           pph[0] ^= 1u;
           ptx::tc_fence_after();
@@ -608,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
               TRACE_MM(16, nitem);
             }
             TRACE_MM(18, j);
-            MMA_WAIT(&kv_full[kslot1], kph1);
+            if (!TA_EARLY_K) MMA_WAIT(&kv_full[kslot1], kph1);
             ptx::tc_fence_after();
             TRACE_MM(19, j);
             issue_qk(0, kslot1, f1, b1);
@@ -644,11 +680,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       }
     }
     __syncwarp();
-  } else if (warp < kSoftmaxWarps) {
+  } else if (warp >= kSmWarp0 && warp < kSmWarp0 + kSoftmaxWarps) {
     // ===================== softmax / epilogue =====================
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax) : "memory");
-    const int x = warp / (4 * kHPR);    // Q tile
-    const int hc = (warp / 4) % kHPR;   // column part: S columns [kNCol hc, kNCol (hc + 1))
+    const int x = (warp - kSmWarp0) / (4 * kHPR);    // Q tile
+    const int hc = ((warp - kSmWarp0) / 4) % kHPR;   // column part: S columns [kNCol hc, kNCol (hc + 1))
     const int wq = warp % 4;            // TMEM lane quarter
     const int r = wq * 32 + lane;       // packed row = TMEM lane
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
@@ -826,6 +862,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         // alternate, so each runs at full SMSP throughput while the tensor core works on
         // the other tile.
         if (kPingPong) ptx::mbar_wait(&exp_turn[x], (ecount & 1u) ^ (x == 0 ? 1u : 0u));
+        spin_cycles(TA_DELAY_SM);
         const uint64_t sc2 = f2pack(sc, sc);
         uint64_t nref2 = f2pack(-ref, -ref);
         uint64_t l2a = 0, l2b = 0;  // packed partial row sums (FADD2)
