@@ -156,6 +156,12 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_MMA_REMAT
 #define TA_MMA_REMAT 1
 #endif
+#ifndef TA_EXTRA_WAITS
+#define TA_EXTRA_WAITS 0
+#endif
+#ifndef TA_PV_SPLIT  // PV in two halves, the first on p_ready (keys 0..63) mid-softmax
+#define TA_PV_SPLIT 0
+#endif
 #ifndef TA_EARLY_K
 #define TA_EARLY_K 1
 #endif
@@ -478,18 +484,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           ring_pos(seq, C::kStages, slot, ph);
           ptx::mbar_wait_lazy(&kv_empty[slot], ph ^ 1u);
           if (leader) {
+            uint64_t *const fb = &kv_full[slot];
             // one 128-row box, or 16 sink rows + a 112-row band box (fused first block)
-            ptx::mbar_arrive_expect_tx(&kv_full[slot], kBlockKeys * 128 * C::kHalves);
+            ptx::mbar_arrive_expect_tx(fb, kBlockKeys * 128 * C::kHalves);
             uint8_t *dst = sKV + slot * C::kSlotBytes;
             for (int h = 0; h < C::kHalves; ++h) {
               if (b.sink) {
                 ptx::tma_load_3d(dst + h * C::kSlotHalfBytes, kv ? &p.tm_vs : &p.tm_ks,
-                                 &kv_full[slot], h * 64, 0, f.kvh);
+                                 fb, h * 64, 0, f.kvh);
                 ptx::tma_load_3d(dst + h * C::kSlotHalfBytes + kSinkRows * 128,
-                                 kv ? &p.tm_vb : &p.tm_kb, &kv_full[slot], h * 64, b.kb, f.kvh);
+                                 kv ? &p.tm_vb : &p.tm_kb, fb, h * 64, b.kb, f.kvh);
               } else {
                 ptx::tma_load_3d(dst + h * C::kSlotHalfBytes, kv ? &p.tm_v : &p.tm_k,
-                                 &kv_full[slot], h * 64, b.kb, f.kvh);
+                                 fb, h * 64, b.kb, f.kvh);
               }
             }
             TRACE_PR(2 + kv, j);
@@ -603,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           ring_pos(seq + 1, C::kStages, vslot, vph);
           TRACE_MM(9, j);
           MMA_WAIT(&kv_full[vslot], vph);
+          for (int w = 0; w < TA_EXTRA_WAITS; ++w) MMA_WAIT(&kv_full[vslot], vph);
           TRACE_MM(17, j);
           // next block in the flat stream (same item j+1, or block 0 of the next item)
           const bool last = (j + 1 == f.nb);
@@ -625,15 +633,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           // ---- tile A: PV_A(j), then QK_A(next)
           TRACE_MM(8, j);
           spin_cycles(TA_DELAY_MMA);
-          MMA_WAIT(&p_ready[0], pph[0]);
-          pph[0] ^= 1u;
-          ptx::tc_fence_after();
+          if (TA_PV_SPLIT) {
+            MMA_WAIT(&p_ready[0], pph[0]);
+            pph[0] ^= 1u;
+            ptx::tc_fence_after();
+          }
           TRACE_MM(10, j);
           const uint32_t kitem = ii - it_beg;  // item of block j
           if (j == 0 && kitem > 0) MMA_WAIT(&o_free[0], (kitem - 1) & 1u);  // O_A drained
-          issue_pv(0, vslot, f, b, j > 0, 0);   // keys 0..63 while the softmax finishes 64..127
-          MMA_WAIT(&p_hi[0], pph[0] ^ 1u);
+          if (TA_PV_SPLIT) {
+            issue_pv(0, vslot, f, b, j > 0, 0);  // keys 0..63 while the softmax finishes 64..127
+            MMA_WAIT(&p_hi[0], pph[0] ^ 1u);
+          } else {
+            MMA_WAIT(&p_hi[0], pph[0]);
+            pph[0] ^= 1u;
+          }
           ptx::tc_fence_after();
+          if (!TA_PV_SPLIT) issue_pv(0, vslot, f, b, j > 0, 0);
           issue_pv(0, vslot, f, b, j > 0, 4);
           TRACE_MM(11, j);
           if (last) commit(&o_full[0]);
@@ -653,14 +669,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           // ---- tile B: PV_B(j), then QK_B(next)
           TRACE_MM(7, j);
-          MMA_WAIT(&p_ready[1], pph[1]);
-          pph[1] ^= 1u;
-          ptx::tc_fence_after();
+          if (TA_PV_SPLIT) {
+            MMA_WAIT(&p_ready[1], pph[1]);
+            pph[1] ^= 1u;
+            ptx::tc_fence_after();
+          }
           TRACE_MM(13, j);
           if (j == 0 && kitem > 0) MMA_WAIT(&o_free[1], (kitem - 1) & 1u);  // O_B drained
-          issue_pv(1, vslot, f, b, j > 0, 0);
-          MMA_WAIT(&p_hi[1], pph[1] ^ 1u);
+          if (TA_PV_SPLIT) {
+            issue_pv(1, vslot, f, b, j > 0, 0);  // keys 0..63 while the softmax finishes 64..127
+            MMA_WAIT(&p_hi[1], pph[1] ^ 1u);
+          } else {
+            MMA_WAIT(&p_hi[1], pph[1]);
+            pph[1] ^= 1u;
+          }
           ptx::tc_fence_after();
+          if (!TA_PV_SPLIT) issue_pv(1, vslot, f, b, j > 0, 0);
           issue_pv(1, vslot, f, b, j > 0, 4);
           TRACE_MM(14, j);
           if (last) commit(&o_full[1]);
@@ -870,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #pragma unroll
         for (int c = 0; c < kNCol / 16; ++c) {
           if (c >= nch) {
-            if (kHPR == 1 && c == 3) {  // keep the p_ready hand-off when the block is short
+            if (kHPR == 1 && c == 3 && TA_PV_SPLIT) {  // keep the p_ready hand-off when the block is short
               ptx::tmem_wait_st();
               ptx::tc_fence_before();
               sm_arrive(&p_ready[x]);
@@ -907,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             ptx::tmem_st8(tS + c * 8, pk);
           else if (c & 1)  // two chunks (32 keys) per 16-column store
             ptx::tmem_st16(tS + (c - 1) * 8, pkw);
-          if (kHPR == 1 && c == 3) {
+          if (kHPR == 1 && c == 3 && TA_PV_SPLIT) {
             // keys 0..63 of P are in TMEM: the MMA can start PV on them right away
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
