@@ -186,7 +186,7 @@ ta_status encode_map(CUtensorMap *m, const void *data, int64_t n, int heads, int
   return TA_OK;
 }
 
-#ifdef TA_TRACE
+#if defined(TA_TRACE) || defined(TA_CTA_CLOCK)
 unsigned long long *g_trace_buf = nullptr;
 #endif
 
@@ -313,6 +313,14 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
     rec.a1 = take_event();
     cudaEventRecord(rec.a0, stream);
   }
+#if defined(TA_CTA_CLOCK)
+  {  // per-CTA elapsed SM cycles of this launch (kernel-variant comparisons independent of clocks)
+    static unsigned long long *cbuf = nullptr;
+    if (!cbuf) cudaMalloc(&cbuf, sizeof(unsigned long long) * 65536 * 8);
+    prm.trace = cbuf;
+    g_trace_buf = cbuf;
+  }
+#endif
 #ifdef TA_TRACE
   {
     static unsigned long long *tbuf = nullptr;
@@ -532,7 +540,7 @@ ta_status ta_profile_end(double *attn_ms, int64_t *attn_launches, double *merge_
   return st;
 }
 
-#ifdef TA_TRACE
+#if defined(TA_TRACE) || defined(TA_CTA_CLOCK)
 /* Debug build only: copy the last launch's timeline (4 x 65536 u64) to the host. */
 ta_status ta_debug_trace_read(void *host, size_t cap) {
   if (!g_trace_buf) return TA_ERR_CUDA;

@@ -160,10 +160,10 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #define TA_EXTRA_WAITS 0
 #endif
 #ifndef TA_PV_SPLIT  // PV in two halves, the first on p_ready (keys 0..63) mid-softmax
-#define TA_PV_SPLIT 0
+#define TA_PV_SPLIT 1
 #endif
 #ifndef TA_EARLY_K
-#define TA_EARLY_K 1
+#define TA_EARLY_K 0
 #endif
 #ifndef TA_PINGPONG
 #define TA_PINGPONG 0
@@ -443,6 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+#ifdef TA_CTA_CLOCK
+  const long long cta_t0 = clock64();
+#endif
   const uint32_t it_beg = p.offsets[blockIdx.x];
   const uint32_t it_end = p.offsets[blockIdx.x + 1];
 
@@ -1070,6 +1073,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   }
   if (threadIdx.x == kEpiWarp0 * 32) ptx::bulk_wait0();  // epilogue TMA stores complete
   __syncthreads();
+#ifdef TA_CTA_CLOCK
+  if (threadIdx.x == 0) p.trace[blockIdx.x] = (unsigned long long)(clock64() - cta_t0);
+#endif
   if (warp == kAllocWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);

@@ -15,10 +15,11 @@ for r in range(rounds):
                               "--steps", "30"] + args, env=env, capture_output=True, text=True)
         try:
             d = json.loads(out.stdout.strip().splitlines()[-1])
-            res[os.path.basename(so)].append((round(d["ms_per_layer"], 4), d.get("dense_ms_per_layer")))
+            res[os.path.basename(so)].append((round(d["ms_per_layer"], 4), d.get("dense_ms_per_layer"),
+                                              d.get("clocks", {}).get("sm_mhz"), round(d["kernel_ms"]["attn"], 4)))
         except Exception:
             res[os.path.basename(so)].append(("ERR", out.stderr[-300:]))
 for k, v in res.items():
     ok = [x for x in v if x[0] != "ERR"]
     best = min(ok) if ok else v
-    print(k, "min", best, "all", [x[0] for x in v], flush=True)
+    print(k, "min", best, "all", [(x[0], x[2]) if len(x) > 2 else x[0] for x in v], flush=True)
