@@ -138,7 +138,7 @@ constexpr int kEmpty = 1 << 30;            // canonical empty column interval [k
 #define TA_POLY_DEG 3
 #endif
 #ifndef TA_POLY_MASK
-#define TA_POLY_MASK 0x00
+#define TA_POLY_MASK 0x01
 #endif
 constexpr int kPolyPairs = TA_POLY_MASK;
 // MMA issuer barrier waits: suspending try_wait (default) or a test_wait spin
@@ -148,7 +148,7 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #define MMA_WAIT(bar, ph) ptx::mbar_wait(bar, ph)
 #endif
 #ifndef TA_TMEM_WIDE
-#define TA_TMEM_WIDE 0
+#define TA_TMEM_WIDE 1
 #endif
 #ifndef TA_EXP_ORDER
 #define TA_EXP_ORDER 1
