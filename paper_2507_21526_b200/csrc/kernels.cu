@@ -10,13 +10,13 @@
 //                   thread straight out of TMEM.
 //  merge_kernel<D>  LSE merge of the split-K partials (merge_output).
 //
-// CTA layout (384 threads, 1 CTA per SM):
-//   warp 0      TMA producer (one elected lane)
-//   warp 1      MMA issuer  (one elected lane)
-//   warp 2      TMEM allocator
-//   warp 3      idle
-//   warps 4-7   softmax/epilogue for Q tile A (TMEM lanes 0-127)
-//   warps 8-11  softmax/epilogue for Q tile B
+// CTA layout (512 threads, 1 CTA per SM):
+//   warps 0-3   epilogue warpgroup (O normalisation + TMA stores, both tiles in turn)
+//   warps 4-7   softmax for Q tile A (TMEM lanes 0-127)
+//   warps 8-11  softmax for Q tile B
+//   warp 12     MMA issuer  (whole warp, one elected lane issues)
+//   warp 13     TMA producer
+//   warp 14     TMEM allocator, warp 15 idle
 // Each item is two GQA-packed Q tiles of 128 rows (G heads x T tokens) that share
 // every K/V block in shared memory.  TMEM (512 columns): S_A [0,128) S_B [128,256)
 // O_A [256,384) O_B [384,512); P (bf16) is written over its S columns and fed to the
@@ -1058,6 +1058,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             asm volatile("bar.sync 5, 128;" ::: "memory");
             if (threadIdx.x == kEpiWarp0 * 32) {
               ptx::tma_store_3d(&p.tm_o, stage, hb * 64, f.r0 + x * T, f.kvh * p.group);
+              // f2: the same staged tile to every extra destination (peer ranks' O)
+              for (int e = 0; e < p.n_ox; ++e)
+                ptx::tma_store_3d(&p.tm_ox[e], stage, hb * 64, f.r0 + x * T, f.kvh * p.group);
               ptx::bulk_commit();
             }
           }
@@ -1129,6 +1132,12 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Attn
                        (int64_t)orow * p.o_st;
 #pragma unroll
   for (int e = 0; e < E; ++e) dst[lane + 32 * e] = __float2bfloat16_rn(acc[e] * inv);
+  for (int x2 = 0; x2 < p.n_ox; ++x2) {  // f2: extra destinations
+    __nv_bfloat16 *d2 = reinterpret_cast<__nv_bfloat16 *>(p.ox[x2]) + (int64_t)head * p.ox_sh[x2] +
+                        (int64_t)orow * p.ox_st[x2];
+#pragma unroll
+    for (int e = 0; e < E; ++e) d2[lane + 32 * e] = __float2bfloat16_rn(acc[e] * inv);
+  }
   if (lane == 0 && p.lse)
     p.lse[(int64_t)head * (p.n - p.o_row0) + orow] = wsum > 0.f ? mx + __logf(wsum) : -INFINITY;
 }
