@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define TA_ABI_VERSION 2  /* v2: last_q = 0 (StreamingMix), final-layer last-rows entry points */
+#define TA_ABI_VERSION 3  /* v2: last_q = 0 (StreamingMix), final-layer last-rows entry points; v3: *_multi (f2) */
 
 /* Same type as the CUDA runtime's cudaStream_t (a duplicate identical typedef is
  * legal in C11/C++), so callers need no CUDA headers. NULL = legacy stream. */
@@ -122,6 +122,30 @@ ta_status dense_attn_prefill(const ta_problem *p, void *ws, size_t ws_bytes,
 ta_status ta_layer_attn_prefill(int32_t layer, int32_t tri_start, const ta_problem *p,
                                 const ta_triangle *tri, void *ws, size_t ws_bytes,
                                 cudaStream_t stream);
+
+/* ---- fused output replication ---------------------- *
+ * Multi-GPU head sharding: rank r owns kv heads [r Hkv/P, (r+1) Hkv/P) and their q heads,
+ * and every rank needs the full O [Hq][N][d] (the all-gather of 8(a) a7).  These calls run
+ * the same kernels as triangle_attn_prefill / dense_attn_prefill, and the epilogue writes
+ * each finished bf16 O tile, with the same TMA tensor store, to p->o AND to n_extra further
+ * destinations extra_o[0..n_extra): typically this rank's head slice of the other ranks'
+ * full-O buffers, mapped into this process (CUDA IPC / symmetric memory over NVLink), so
+ * the gather overlaps the attention tile by tile instead of following it.  The LSE merge of
+ * the last rows writes them to every destination as well.
+ *   extra_o[e]: device pointer + strides of a bf16 [Hq][N][d] view (the same Hq heads
+ *               and rows as p->o), 16-B aligned like p->o; caller-owned.
+ *   0 <= n_extra <= TA_MAX_EXTRA_OUT; n_extra == 0 is exactly triangle_attn_prefill.
+ * Visibility on the peers is the caller's business: after the call completes on this
+ * rank's stream, a cross-rank barrier (e.g. symmetric-memory barrier or NCCL) must order
+ * it before peers read their buffers.  Errors: TA_ERR_NULL_ARG (extra_o NULL with
+ * n_extra > 0, or a NULL data pointer), TA_ERR_PARAMS (n_extra out of range),
+ * TA_ERR_UNSUPPORTED (misaligned pointer / stride), as for p->o. */
+#define TA_MAX_EXTRA_OUT 7
+ta_status triangle_attn_prefill_multi(const ta_problem *p, const ta_triangle *tri,
+                                      const ta_out_tensor *extra_o, int32_t n_extra, void *ws,
+                                      size_t ws_bytes, cudaStream_t stream);
+ta_status dense_attn_prefill_multi(const ta_problem *p, const ta_out_tensor *extra_o,
+                                   int32_t n_extra, void *ws, size_t ws_bytes, cudaStream_t stream);
 
 /* ---- final layer: last query rows only ----------------------- *
  * "For the last layer, only the last r rows of the attention output are needed"

@@ -25,6 +25,7 @@ import os
 __all__ = [
     "TriattnError", "triangle_attn_prefill", "dense_attn_prefill", "layer_attn_prefill",
     "workspace_size", "pair_count", "schedule_export", "abi_version", "release_caches",
+    "triangle_attn_prefill_multi", "dense_attn_prefill_multi",
     "library_path", "STATUS", "profile_begin", "profile_end", "last_rows_attn_prefill",
     "last_rows_workspace_size", "last_rows_schedule_export",
 ]
@@ -83,6 +84,10 @@ def _load():
     lib.triangle_attn_prefill.restype = ctypes.c_int
     lib.dense_attn_prefill.argtypes = [P, vp, sz, vp]
     lib.dense_attn_prefill.restype = ctypes.c_int
+    lib.triangle_attn_prefill_multi.argtypes = [P, Tp, vp, ctypes.c_int32, vp, sz, vp]
+    lib.triangle_attn_prefill_multi.restype = ctypes.c_int
+    lib.dense_attn_prefill_multi.argtypes = [P, vp, ctypes.c_int32, vp, sz, vp]
+    lib.dense_attn_prefill_multi.restype = ctypes.c_int
     lib.ta_layer_attn_prefill.argtypes = [ctypes.c_int32, ctypes.c_int32, P, Tp, vp, sz, vp]
     lib.ta_layer_attn_prefill.restype = ctypes.c_int
     lib.ta_pair_count.argtypes = [ctypes.c_int64, Tp, ctypes.POINTER(ctypes.c_int64)]
@@ -186,6 +191,50 @@ def triangle_attn_prefill(q, k, v, o=None, *, sink: int = 8, window: int = 512, 
     ws, need = _workspace(p, tri, q.device)
     _check(_load().triangle_attn_prefill(ctypes.byref(p), ctypes.byref(tri), ws, need,
                                          _stream(stream)))
+    return o
+
+
+def _extra_views(extra_out, like):
+    """ctypes array of ta_out_tensor views of the extra destinations (f2), each checked like o."""
+    import torch
+    n = len(extra_out)
+    arr = (_InTensor * max(n, 1))()
+    for e, t in enumerate(extra_out):
+        if (t.dtype != torch.bfloat16 or t.dim() != 3 or not t.is_cuda or t.stride(2) != 1
+                or tuple(t.shape) != tuple(like.shape)):
+            raise TriattnError(3, f"extra_out[{e}]: need a CUDA bf16 view shaped like o, d-stride 1")
+        arr[e] = _view(t)
+    return arr, n
+
+
+def triangle_attn_prefill_multi(q, k, v, extra_out, o=None, *, sink: int = 8, window: int = 512,
+                                last_q: int = 128, lse=None, scale: float = 0.0, stream=None):
+    """triangle_attn_prefill whose epilogue also writes every O tile to each tensor of
+    extra_out (f2: e.g. this rank's head slice of peer ranks' full-O buffers); returns o."""
+    import torch
+    if o is None:
+        o = torch.empty_like(q)
+    _check_tensors(q, k, v, o, lse)
+    arr, n = _extra_views(extra_out, o)
+    p = _problem(q, k, v, o, lse, scale)
+    tri = _Triangle(sink, window, last_q)
+    ws, need = _workspace(p, tri, q.device)
+    _check(_load().triangle_attn_prefill_multi(ctypes.byref(p), ctypes.byref(tri), arr, n, ws, need,
+                                               _stream(stream)))
+    return o
+
+
+def dense_attn_prefill_multi(q, k, v, extra_out, o=None, *, lse=None, scale: float = 0.0,
+                             stream=None):
+    """dense_attn_prefill with the f2 extra output destinations; returns o."""
+    import torch
+    if o is None:
+        o = torch.empty_like(q)
+    _check_tensors(q, k, v, o, lse)
+    arr, n = _extra_views(extra_out, o)
+    p = _problem(q, k, v, o, lse, scale)
+    ws, need = _workspace(p, None, q.device)
+    _check(_load().dense_attn_prefill_multi(ctypes.byref(p), arr, n, ws, need, _stream(stream)))
     return o
 
 

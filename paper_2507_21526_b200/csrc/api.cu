@@ -225,7 +225,8 @@ bool call_geometry(const ta_problem *p, const ta_triangle *tri, Mode mode, int32
 }
 
 ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t last_q, void *ws,
-              size_t ws_bytes, cudaStream_t stream) {
+              size_t ws_bytes, cudaStream_t stream, const ta_out_tensor *extra_o = nullptr,
+              int32_t n_extra = 0) {
   const bool dense = mode == kDenseMode;
   ta_status s = validate_shape(p);
   if (s != TA_OK) return s;
@@ -233,6 +234,15 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
   const int64_t o_rows = mode == kLastRows ? std::min<int64_t>(last_q, p->seq_len) : p->seq_len;
   if ((s = validate_problem(p, o_rows)) != TA_OK) return s;
   if (mode == kTriangle && (s = validate_triangle(tri)) != TA_OK) return s;
+  // f2: extra output destinations, validated like p->o before anything is enqueued
+  if (n_extra < 0 || n_extra > ta::kMaxExtraOut || (n_extra > 0 && mode == kLastRows))
+    return fail(TA_ERR_PARAMS, "n_extra must be in [0, " + std::to_string(ta::kMaxExtraOut) +
+                                   "] (and 0 for the last-rows mode)");
+  if (n_extra > 0 && !extra_o) return fail(TA_ERR_NULL_ARG, "extra_o is NULL");
+  for (int e = 0; e < n_extra; ++e)
+    if ((s = validate_tensor("extra_o", extra_o[e].data, extra_o[e].stride_head,
+                             extra_o[e].stride_token, p->num_q_heads, o_rows, p->head_dim)))
+      return s;
   int dev;
   DeviceInfo di;
   if ((s = device_info(&dev, &di)) != TA_OK) return s;
@@ -277,6 +287,15 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
   prm.o = p->o.data;
   prm.o_sh = p->o.stride_head;
   prm.o_st = p->o.stride_token;
+  prm.n_ox = n_extra;
+  for (int e = 0; e < n_extra; ++e) {
+    if ((s = encode_map(&prm.tm_ox[e], extra_o[e].data, o_rows, g.hq, g.d, extra_o[e].stride_head,
+                        extra_o[e].stride_token, T, G)))
+      return s;
+    prm.ox[e] = extra_o[e].data;
+    prm.ox_sh[e] = extra_o[e].stride_head;
+    prm.ox_st[e] = extra_o[e].stride_token;
+  }
   prm.lse = p->lse;
   if (need > 0) {
     const int64_t slots = ta::num_partial_slots(ds.g);
@@ -382,6 +401,30 @@ ta_status triangle_attn_prefill(const ta_problem *p, const ta_triangle *tri, voi
   try {
     if (!tri) return fail(TA_ERR_NULL_ARG, "triangle parameters are NULL");
     return run(p, tri, kTriangle, 0, ws, ws_bytes, stream);
+  } catch (const std::exception &ex) {
+    return fail(TA_ERR_CUDA, ex.what());
+  } catch (...) {
+    return fail(TA_ERR_CUDA, "unknown exception");
+  }
+}
+
+ta_status triangle_attn_prefill_multi(const ta_problem *p, const ta_triangle *tri,
+                                      const ta_out_tensor *extra_o, int32_t n_extra, void *ws,
+                                      size_t ws_bytes, cudaStream_t stream) {
+  try {
+    if (!tri) return fail(TA_ERR_NULL_ARG, "triangle parameters are NULL");
+    return run(p, tri, kTriangle, 0, ws, ws_bytes, stream, extra_o, n_extra);
+  } catch (const std::exception &ex) {
+    return fail(TA_ERR_CUDA, ex.what());
+  } catch (...) {
+    return fail(TA_ERR_CUDA, "unknown exception");
+  }
+}
+
+ta_status dense_attn_prefill_multi(const ta_problem *p, const ta_out_tensor *extra_o,
+                                   int32_t n_extra, void *ws, size_t ws_bytes, cudaStream_t stream) {
+  try {
+    return run(p, nullptr, kDenseMode, 0, ws, ws_bytes, stream, extra_o, n_extra);
   } catch (const std::exception &ex) {
     return fail(TA_ERR_CUDA, ex.what());
   } catch (...) {

@@ -9,6 +9,8 @@
 
 namespace ta {
 
+constexpr int kMaxExtraOut = 7;  // TA_MAX_EXTRA_OUT
+
 // Passed by value as a __grid_constant__ kernel parameter; the TMA descriptors
 // must live in param space so cp.async.bulk.tensor can take their address.
 struct alignas(64) AttnParams {
@@ -36,6 +38,11 @@ struct alignas(64) AttnParams {
   float scale;       // softmax_scale
   unsigned long long *trace;  // debug timeline (TA_TRACE builds only), else NULL
   int trace_cta;
+  // f2: extra output destinations (triangle/dense_attn_prefill_multi), same layout as O
+  int n_ox;
+  void *ox[kMaxExtraOut];
+  int64_t ox_sh[kMaxExtraOut], ox_st[kMaxExtraOut];
+  CUtensorMap tm_ox[kMaxExtraOut];
 };
 
 // Launchers (kernels.cu). Return the CUDA error of the launch.

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert ta.abi_version() == 2
+    assert ta.abi_version() == 3
 
 
 def test_status_strings():
@@ -137,3 +137,22 @@ def test_graft_entry_build():
     sys.path.insert(0, ROOT)
     g = importlib.import_module("__graft_entry__")
     g.build()
+
+
+def test_multi_destination_validation_without_gpu():
+    """f2 entry points: n_extra range and NULL destinations are rejected before any CUDA call."""
+    lib = ta._load()
+    p = ta._shape_problem(64, 32, 8, 128)
+    fake = 1 << 20  # aligned, never dereferenced on the host
+    for t in ("q", "o"):
+        setattr(p, t, ta._InTensor(fake, 64 * 128, 128))
+    for t in ("k", "v"):
+        setattr(p, t, ta._InTensor(fake, 64 * 128, 128))
+    tri = ta._Triangle(8, 512, 128)
+    arr = (ta._InTensor * 8)(*[ta._InTensor(fake, 64 * 128, 128) for _ in range(8)])
+    assert lib.triangle_attn_prefill_multi(ctypes.byref(p), ctypes.byref(tri), arr, 8, None, 0, None) == 4
+    assert lib.triangle_attn_prefill_multi(ctypes.byref(p), ctypes.byref(tri), arr, -1, None, 0, None) == 4
+    assert lib.triangle_attn_prefill_multi(ctypes.byref(p), ctypes.byref(tri), None, 1, None, 0, None) == 1
+    arr[0] = ta._InTensor(0, 64 * 128, 128)
+    assert lib.dense_attn_prefill_multi(ctypes.byref(p), arr, 1, None, 0, None) == 1
+    assert "extra_o" in lib.ta_last_error().decode()

@@ -259,3 +259,46 @@ def test_synthetic_prefill_model_matches_cpu_reference():
     # the final-layer last-rows mode gives the same last rows
     y2 = m.forward(x.to(dev), sink=si, window=sl, last_q=last, final_last_rows=True).float().cpu()
     assert (y2 - y).abs().max().item() <= 0.05 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_multi_destination_output(dense):
+    """f2: the *_multi entry points write every O tile, and the merged last
+    rows, to p->o and to each extra destination (here local buffers standing in for peer
+    ranks' full-O buffers, one of them a strided head slice of a larger token-major tensor);
+    all copies are bitwise the single-output result, which matches the oracle."""
+    hq, hkv, n, d, si, sl, last = 32, 8, 2049, 128, 8, 512, 128
+    q, k, v = synth.make_qkv(hq, hkv, n, d, 11, "iid", si)
+    dev = torch.device("cuda")
+    qd, kd, vd = q.to(dev), k.to(dev), v.to(dev)
+    ref = torch.empty_like(qd)
+    if dense:
+        ta.dense_attn_prefill(qd, kd, vd, ref)
+    else:
+        ta.triangle_attn_prefill(qd, kd, vd, ref, sink=si, window=sl, last_q=last)
+    big = torch.full((n, 2 * hq, d), float("nan"), dtype=torch.bfloat16, device=dev)
+    extras = [torch.full_like(qd, float("nan")) for _ in range(2)]
+    extras.append(big[:, hq:, :].permute(1, 0, 2))  # token-major rows of another "rank"
+    o = torch.full_like(qd, float("nan"))
+    if dense:
+        ta.dense_attn_prefill_multi(qd, kd, vd, extras, o)
+    else:
+        ta.triangle_attn_prefill_multi(qd, kd, vd, extras, o, sink=si, window=sl, last_q=last)
+    torch.cuda.synchronize()
+    assert torch.equal(o, ref)
+    for e in extras:
+        assert torch.equal(e, ref)
+    assert torch.isnan(big[:, :hq, :].float()).all()  # nothing outside the destination views
+    o_ref, _, _ = cref.attention(q, k, v, si, sl, last, dense)
+    _compare(o.float().cpu(), o_ref, "multi")
+
+
+def test_multi_destination_errors():
+    q, k, v = (torch.zeros((4, 64, 128), dtype=torch.bfloat16, device="cuda") for _ in range(3))
+    o = torch.zeros_like(q)
+    with pytest.raises(ta.TriattnError) as e:
+        ta.triangle_attn_prefill_multi(q, k[:1], v[:1], [torch.zeros_like(q)] * 8, o)
+    assert e.value.status == 4  # TA_ERR_PARAMS: more than TA_MAX_EXTRA_OUT
+    with pytest.raises(ta.TriattnError):
+        ta.triangle_attn_prefill_multi(q, k[:1], v[:1], [torch.zeros((4, 63, 128), dtype=torch.bfloat16,
+                                                                     device="cuda")], o)
