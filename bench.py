@@ -48,6 +48,11 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time C2/C4a/C4b (extra JSON key)")
+    ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
+                    help="N>1: O all-gather by NCCL after the kernel, or fused into the kernel "
+                         "epilogue (f2: *_multi entry points storing into peer ranks' symmetric-"
+                         "memory O buffers over NVLink; checked against NCCL once, falls back "
+                         "to NCCL if the symmetric-memory rendezvous or the check fails)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     return ap.parse_args()
 
@@ -231,13 +236,48 @@ def main():
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def layer(dense=False):
+    def layer_nccl(dense=False):
         if dense:
             ta.dense_attn_prefill(qd, kd, vd, od)
         else:
             ta.triangle_attn_prefill(qd, kd, vd, od, sink=c.si, window=c.sl, last_q=c.last)
         if world > 1:
             shard.gather_heads(od, world, out=o_full, plan=plan)
+
+    layer = layer_nccl
+    gather_mode = "nccl" if world > 1 else None
+    if world > 1 and args.gather == "fused":
+        # f2: every rank's epilogue stores its O tiles into all ranks' symmetric-memory
+        # full-O buffers (own slice + the same head slice of each peer); a device-side
+        # barrier orders them before the next layer reads.  Verified once against NCCL.
+        try:
+            import torch.distributed._symmetric_memory as symm
+            o_sym = symm.empty((c.hq, c.n, c.d), dtype=torch.bfloat16, device=dev)
+            hdl = symm.rendezvous(o_sym, dist.group.WORLD)
+            h0, h1 = plan[rank][2], plan[rank][3]
+            peers = [hdl.get_buffer(r, (c.hq, c.n, c.d), torch.bfloat16)[h0:h1]
+                     for r in range(world) if r != rank]
+            own = o_sym[h0:h1]
+
+            def layer_fused(dense=False):
+                if dense:
+                    ta.dense_attn_prefill_multi(qd, kd, vd, peers, own)
+                else:
+                    ta.triangle_attn_prefill_multi(qd, kd, vd, peers, own, sink=c.si, window=c.sl,
+                                                   last_q=c.last)
+                hdl.barrier(channel=0)
+
+            layer_nccl()
+            layer_fused()
+            torch.cuda.synchronize()
+            ok = torch.tensor([1.0 if torch.equal(o_sym, o_full) else 0.0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() == 1.0:
+                layer, gather_mode = layer_fused, "fused (kernel epilogue -> peer symmetric memory)"
+            else:
+                gather_mode = "nccl (fused output check failed)"
+        except Exception as e:  # no P2P / symmetric memory on this box: report and keep NCCL
+            gather_mode = f"nccl (fused unavailable: {type(e).__name__}: {str(e)[:120]})"
 
     def barrier():
         torch.cuda.synchronize()
@@ -418,7 +458,7 @@ def main():
                        "global_batch": 1, "seq_len": c.n,
                        "parallelism": (f"kv-head shard x{world}" if world <= c.hkv else
                                        f"q-head split x{world} ({world // c.hkv} ranks per kv head)")
-                                      + (" + NCCL all-gather of O" if world > 1 else ""),
+                                      + (f" + O all-gather: {gather_mode}" if world > 1 else ""),
                        "l2": "flushed (512 MiB write) before every timed step; inputs 1.5 GB > L2"},
             "ms_per_layer": ms_tri,
             "dense_ms_per_layer": dense_ms,
