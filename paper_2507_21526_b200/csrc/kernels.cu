@@ -1050,9 +1050,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 pk[c * 8 + e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv,
                                                __uint_as_float(ov[2 * e + 1]) * inv);
             }
+            TRACE_EP(40 + hb, kitem);
             // staging buffer free: the previous TMA store has finished reading it
             if (threadIdx.x == kEpiWarp0 * 32) ptx::bulk_wait_read0();
             asm volatile("bar.sync 5, 128;" ::: "memory");
+            TRACE_EP(42 + hb, kitem);
 #pragma unroll
             for (int pc = 0; pc < 8; ++pc)
               sts_v4(stage_s + r * 128 + ((pc ^ (r & 7)) << 4), pk[4 * pc], pk[4 * pc + 1],
@@ -1067,6 +1069,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                   ptx::tma_store_3d(&p.tm_ox[e], stage, hb * 64, f.r0 + x * T, f.kvh * p.group);
               ptx::bulk_commit();
             }
+            TRACE_EP(44 + hb, kitem);
           }
           if (valid && p.lse) p.lse[(int64_t)head * p.n + tok] = lse;
         }
