@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time C2/C4a/C4b (extra JSON key)")
+    ap.add_argument("--l2", choices=["flush", "inputs"], default="flush",
+                    help="between timed steps: write a 512 MiB buffer (flush), or rely on the "
+                         "inputs (1.5 GB at C3) exceeding the 126 MB L2 (inputs)")
     ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
                     help="N>1: O all-gather by NCCL after the kernel, or fused into the kernel "
                          "epilogue (f2: *_multi entry points storing into peer ranks' symmetric-"
@@ -299,7 +302,8 @@ def main():
         if profile:
             ta.profile_begin()
         for s in range(steps):
-            flush.zero_()                 # L2 flush between timed iterations (> 126 MB L2)
+            if args.l2 == "flush":
+                flush.zero_()             # L2 flush between timed iterations (> 126 MB L2)
             evs[s][0].record(stream)
             layer(dense)
             evs[s][1].record(stream)
@@ -459,7 +463,9 @@ def main():
                        "parallelism": (f"kv-head shard x{world}" if world <= c.hkv else
                                        f"q-head split x{world} ({world // c.hkv} ranks per kv head)")
                                       + (f" + O all-gather: {gather_mode}" if world > 1 else ""),
-                       "l2": "flushed (512 MiB write) before every timed step; inputs 1.5 GB > L2"},
+                       "l2": ("flushed (512 MiB write) before every timed step; inputs 1.5 GB > L2"
+                              if args.l2 == "flush" else
+                              "no flush: inputs (Q/K/V/O 1.5 GB at C3) exceed the 126 MB L2")},
             "ms_per_layer": ms_tri,
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms_tri) if dense_ms else None,
