@@ -16,8 +16,8 @@ Spec summary:
     LASTQ(kvh, p, c): [c*ck, min((c+1)*ck, r1+1)) for c < ceil((r1+1)/ck).
   dense: DENSE(kvh, p) = [0, r1+1).
   blocks: each key range cut at 128, width rounded up to 16; STREAM sink range first.
-  cost = sum of block widths + 64.
-  ck = largest power of two <= C_tot // (4 num_ctas) clamped to [512, 16384]
+  cost = sum of block widths + 192 (per-item overhead: epilogue, pipeline turn-around).
+  ck = largest power of two <= C_tot // (8 num_ctas) clamped to [512, 16384]
        (C_tot: all STREAM items + one unsplit LASTQ item per last pair, all kv heads).
   canonical order: LASTQ (kvh, p, c) then STREAM/DENSE (kvh, p);
   LPT: stable sort by cost descending; each to least-loaded CTA, ties lowest id.
@@ -31,6 +31,10 @@ import struct
 STREAM, LASTQ, DENSE = 0, 1, 2
 MAGIC, VERSION = 0x43534154, 1
 
+
+
+ITEM_OVERHEAD = 192  # LPT cost of an item beyond its key columns
+CK_DIV = 8           # chunk_keys target: C_tot / (CK_DIV * num_ctas)
 
 def _r16(x):
     return -(-x // 16) * 16
@@ -89,7 +93,7 @@ def item_blocks(geo, it):
 
 
 def cost(geo, it):
-    return sum(b[2] for b in item_blocks(geo, it)) + 64
+    return sum(b[2] for b in item_blocks(geo, it)) + ITEM_OVERHEAD
 
 
 def stream_item(geo, kvh, p):
@@ -108,7 +112,7 @@ def chunk_keys(geo, num_ctas):
     for p in range(geo["p_last0"], geo["pairs"]):
         tot += cost(geo, (LASTQ, 0, p, 0, rows(geo, p)[1] + 1))
     tot *= geo["hkv"]
-    target = tot // (4 * num_ctas)
+    target = tot // (CK_DIV * num_ctas)
     ck = 512
     while ck * 2 <= target and ck * 2 <= 16384:
         ck *= 2

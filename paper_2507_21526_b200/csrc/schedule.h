@@ -35,7 +35,10 @@ constexpr int kTilesPerItem = 2;    // Q tiles sharing one K/V stream (two softm
 constexpr int kBlockKeys = 128;     // max keys per K/V block (tcgen05 N of QK^T)
 constexpr int kKeyGranule = 16;     // MMA N granularity for M=128
 constexpr int kSinkRows = 16;       // sink keys folded into a STREAM item's first block
-constexpr int kItemOverhead = 64;   // LPT cost of an item beyond its key columns (epilogue)
+// LPT cost of an item beyond its key columns (epilogue, pipeline turn-around; measured:
+// a 5-block STREAM item costs about 190 columns more than its blocks inside a long item)
+constexpr int kItemOverhead = 192;
+constexpr int kChunkDiv = 8;  // chunk_keys target: C_tot / (kChunkDiv * num_ctas)
 constexpr uint32_t kScheduleMagic = 0x43534154u;  // "TASC"
 constexpr uint32_t kScheduleVersion = 1;
 
