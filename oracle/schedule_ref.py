@@ -18,6 +18,7 @@ Spec summary:
   blocks: each key range cut at 128, width rounded up to 16; STREAM sink range first.
   cost = sum of block widths + 192 (per-item overhead: epilogue, pipeline turn-around).
   ck = largest power of two <= C_tot // (8 num_ctas) clamped to [512, 16384]
+       (4 num_ctas in the last-rows mode)
        (C_tot: all STREAM items + one unsplit LASTQ item per last pair, all kv heads).
   canonical order: LASTQ (kvh, p, c) then STREAM/DENSE (kvh, p);
   LPT: stable sort by cost descending; each to least-loaded CTA, ties lowest id.
@@ -35,6 +36,7 @@ MAGIC, VERSION = 0x43534154, 1
 
 ITEM_OVERHEAD = 192  # LPT cost of an item beyond its key columns
 CK_DIV = 8           # chunk_keys target: C_tot / (CK_DIV * num_ctas)
+CK_DIV_LAST_ROWS = 4  # ... in the final-layer last-rows mode (LASTQ items only)
 
 def _r16(x):
     return -(-x // 16) * 16
@@ -112,7 +114,7 @@ def chunk_keys(geo, num_ctas):
     for p in range(geo["p_last0"], geo["pairs"]):
         tot += cost(geo, (LASTQ, 0, p, 0, rows(geo, p)[1] + 1))
     tot *= geo["hkv"]
-    target = tot // (CK_DIV * num_ctas)
+    target = tot // ((CK_DIV_LAST_ROWS if geo["last_rows"] else CK_DIV) * num_ctas)
     ck = 512
     while ck * 2 <= target and ck * 2 <= 16384:
         ck *= 2

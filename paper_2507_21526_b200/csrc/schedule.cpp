@@ -119,7 +119,8 @@ void plan_chunks(Geometry *g, int num_ctas) {
     ctot += item_cost(*g, make_item(kLastQ, 0, p, 0, r1 + 1));
   }
   ctot *= g->hkv;
-  int64_t target = ctot / (kChunkDiv * (int64_t)std::max(1, num_ctas));
+  const int64_t div = g->last_only ? kChunkDivLastRows : kChunkDiv;
+  int64_t target = ctot / (div * (int64_t)std::max(1, num_ctas));
   int64_t ck = 512;
   while (ck * 2 <= target && ck * 2 <= 16384) ck *= 2;
   g->chunk_keys = (int)ck;

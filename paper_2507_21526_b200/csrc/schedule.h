@@ -37,8 +37,18 @@ constexpr int kKeyGranule = 16;     // MMA N granularity for M=128
 constexpr int kSinkRows = 16;       // sink keys folded into a STREAM item's first block
 // LPT cost of an item beyond its key columns (epilogue, pipeline turn-around; measured:
 // a 5-block STREAM item costs about 190 columns more than its blocks inside a long item)
-constexpr int kItemOverhead = 192;
-constexpr int kChunkDiv = 8;  // chunk_keys target: C_tot / (kChunkDiv * num_ctas)
+#ifndef TA_ITEM_OVERHEAD  // (overridable for schedule-policy experiments only; the oracle's
+#define TA_ITEM_OVERHEAD 192  // schedule_ref.py mirrors the defaults)
+#endif
+#ifndef TA_CK_DIV
+#define TA_CK_DIV 8
+#endif
+constexpr int kItemOverhead = TA_ITEM_OVERHEAD;
+// chunk_keys target: C_tot / (div * num_ctas); div = kChunkDiv for triangle layers,
+// kChunkDivLastRows for the final-layer last-rows mode (LASTQ items only: finer chunks
+// there only add items and merge work, measured +10 % cycles at C3 with 8)
+constexpr int kChunkDiv = TA_CK_DIV;
+constexpr int kChunkDivLastRows = 4;
 constexpr uint32_t kScheduleMagic = 0x43534154u;  // "TASC"
 constexpr uint32_t kScheduleVersion = 1;
 

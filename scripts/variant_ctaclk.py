@@ -16,8 +16,13 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     lib.ta_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
     mx, mean = [], []
     for r in range(reps + 2):
+        mode = os.environ.get("MODE", "")
         if dense:
             ta.dense_attn_prefill(q, k, v)
+        elif mode == "last":    # f1: final-layer last rows only
+            ta.last_rows_attn_prefill(q, k, v, last_q=c.last)
+        elif mode == "smix":    # f3: StreamingMix layer (last_q = 0)
+            ta.triangle_attn_prefill(q, k, v, sink=c.si, window=c.sl, last_q=0)
         else:
             ta.triangle_attn_prefill(q, k, v, sink=c.si, window=c.sl, last_q=c.last)
         torch.cuda.synchronize()
