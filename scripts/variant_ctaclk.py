@@ -15,7 +15,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     lib = ta._load()
     lib.ta_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
     mx, mean = [], []
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if os.environ.get("FLUSH", "1") == "1" else None
     for r in range(reps + 2):
+        if flush is not None:
+            flush.zero_()  # same L2 state as bench.py's timed steps
         mode = os.environ.get("MODE", "")
         if dense:
             ta.dense_attn_prefill(q, k, v)
