@@ -1124,14 +1124,30 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Attn
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   float wsum = 0.f;
-  for (int c = 0; c < nch; ++c) {
-    const float lc = p.part_lse[(slot0 + c) * rows + rr];
-    if (lc == -INFINITY) continue;  // empty chunk: weight 0, never exp(-inf - -inf)
-    const float w = __expf(lc - mx);
-    wsum += w;
-    const float *src = p.part_o + ((slot0 + c) * rows + rr) * D;
+  // Four chunks per step with all their loads issued first (the merge is latency-bound:
+  // one warp per row, fewer warps than the GPU holds).
+  constexpr int U = 4;
+  for (int c0 = 0; c0 < nch; c0 += U) {
+    float lcs[U], vv[U][E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] += w * src[lane + 32 * e];
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u;
+      lcs[u] = -INFINITY;
+      if (c < nch) {
+        lcs[u] = p.part_lse[(slot0 + c) * rows + rr];
+        const float *src = p.part_o + ((slot0 + c) * rows + rr) * D;
+#pragma unroll
+        for (int e = 0; e < E; ++e) vv[u][e] = src[lane + 32 * e];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (lcs[u] == -INFINITY) continue;  // empty chunk: weight 0, never exp(-inf - -inf)
+      const float w = __expf(lcs[u] - mx);
+      wsum += w;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] += w * vv[u][e];
+    }
   }
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
   const int orow = tok - p.o_row0;
