@@ -470,7 +470,11 @@ def main():
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms_tri) if dense_ms else None,
             "dense_tflops": (kept_flops(c, c.hq, True) / (dense_ms * 1e-3) / 1e12) if dense_ms else None,
+            "dense_frac_of_peak": ((kept_flops(c, c.hq, True) / (dense_ms * 1e-3) / 1e12) / peak
+                                   if dense_ms else None),
             "kernel_ms": {"attn": attn_ms, "merge": merge_ms},
+            # N > 1: the rest of the step is the O all-gather (NCCL, or the fused f2 barrier)
+            "gather_ms": (max(0.0, ms_tri - attn_ms - merge_ms) if world > 1 else None),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
                          "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
