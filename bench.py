@@ -35,6 +35,8 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 
 L2_FLUSH_BYTES = 512 << 20
+# One metric string for both arms (ours and --impl reference) so the driver can pair them.
+METRIC = "triangle-attn prefill kept-FLOP TFLOP/s (ms/layer, speedup vs dense)"
 
 
 def parse():
@@ -57,7 +59,65 @@ def parse():
                          "memory O buffers over NVLink; checked against NCCL once, falls back "
                          "to NCCL if the symmetric-memory rendezvous or the check fails)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-points", action="store_true",
+                    help="skip the C2 / Qwen 64K / Qwen 128K points and the shard-shape points")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch plumbing only (no GPU): every rank joins a gloo group and rank 0 "
+                         "prints the world it saw (tests the --gpus N self-spawn on CPU)")
     return ap.parse_args()
+
+
+def config_dict(args, c, world, gather_mode=None):
+    """The `config` object of the JSON line; identical in both arms (driver pairing)."""
+    if gather_mode is None and world > 1:
+        gather_mode = args.gather if args.gather == "nccl" else "fused"
+    return {"workload": f"{args.workload}: {c.name}, one triangle (deep) layer, "
+                        f"Hq={c.hq} Hkv={c.hkv} d={c.d} si/sl/last={c.si}/{c.sl}/{c.last}",
+            "global_batch": 1, "seq_len": c.n,
+            "parallelism": (f"kv-head shard x{world}" if world <= c.hkv else
+                            f"q-head split x{world} ({world // c.hkv} ranks per kv head)")
+                           + (f" + O all-gather: {gather_mode}" if world > 1 else ""),
+            "l2": ("flushed (512 MiB write) before every timed step; inputs 1.5 GB > L2"
+                   if args.l2 == "flush" else
+                   "no flush: inputs (Q/K/V/O 1.5 GB at C3) exceed the 126 MB L2")}
+
+
+def spawn_if_needed(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun re-executes itself under
+    torch.distributed.run with N ranks; under a launcher the world size must equal --gpus."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def dry_run(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    ranks = [rank]
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        out = [None] * world
+        dist.all_gather_object(out, rank)
+        ranks = out
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": world, "ranks": ranks,
+                          "metric": METRIC}), flush=True)
 
 
 # ------------------------------------------------------------------ helpers
@@ -76,14 +136,17 @@ def measured_peaks():
 
 
 def ncu_traffic():
-    """dram bytes/launch of the attention kernel from the committed ncu --set full summary."""
+    """(dram bytes per launch, source label) of the attention kernel at C3 from the committed
+    `ncu --set full` summary (dram__bytes_read.sum + dram__bytes_write.sum): DRAM counters
+    are not readable from inside the timed run, so the capture is named with its round."""
     path = os.path.join(ROOT, "profiles", "ncu_attn_summary.json")
     if os.path.exists(path):
         try:
-            return json.load(open(path)).get("dram_bytes_per_launch")
+            d = json.load(open(path))
+            return d.get("dram_bytes_per_launch"), d.get("source") or d.get("from")
         except Exception:
-            return None
-    return None
+            return None, None
+    return None, None
 
 
 class ClockSampler:
@@ -167,11 +230,46 @@ def cpu_baseline_run(c, q, k, v, seconds, dense=False):
     _, _, used = cref.attention(q, k, v, c.si, c.sl, c.last, dense, rows=rows, threads=cores)
     dt = time.perf_counter() - t0
     fl = row_flops(rows)
+    fl_all = 4 * c.d * c.hq * (c.n * (c.n + 1) // 2 if dense else
+                                cref.pair_count(c.n, c.si, c.sl, c.last, False))
+    frac = fl / fl_all
     return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": int(used), "kind": "oracle",
             "sample": f"{nrows} uniformly sampled query rows x all {c.hq} q-heads of the "
-                      f"{c.name} {'dense' if dense else 'triangle'} layer (fp64 C oracle, "
-                      f"{dt:.1f} s wall)",
+                      f"{c.name} {'dense' if dense else 'triangle'} layer = {100 * frac:.1f} % of "
+                      f"its kept pairs (fp64 C oracle, {dt:.1f} s wall; whole layer extrapolated "
+                      f"{dt / frac:.0f} s)",
+            "sampled_fraction": frac, "layer_seconds_extrapolated": dt / frac,
             "seconds": dt}
+
+
+def cpu_extra_points(cores):
+    """SURVEY 8(d) oracle timing beside the GPU numbers: C1 triangle and dense in full, C2
+    dense on a bounded row sample (extrapolated by pair count, labelled)."""
+    import numpy as np
+
+    from oracle import cref
+    out = []
+    c1 = synth.CONFIGS["C1"]
+    q, k, v = synth.config_qkv(c1)
+    for dense in (False, True):
+        t0 = time.perf_counter()
+        cref.attention(q, k, v, c1.si, c1.sl, c1.last, dense, threads=1)
+        dt = time.perf_counter() - t0
+        pairs = c1.n * (c1.n + 1) // 2 if dense else cref.pair_count(c1.n, c1.si, c1.sl, c1.last, False)
+        out.append({"workload": f"C1 {'dense' if dense else 'triangle'} (full)", "seconds": dt,
+                    "cores": 1, "mpair_per_s": pairs * c1.hq / dt / 1e6})
+    c2 = synth.CONFIGS["C2"]
+    q, k, v = synth.config_qkv(c2, layer=0)
+    rows = np.sort(np.random.default_rng(7).choice(c2.n, 64, replace=False))
+    t0 = time.perf_counter()
+    _, _, used = cref.attention(q, k, v, 0, 1, 1, True, rows=rows, threads=cores)
+    dt = time.perf_counter() - t0
+    sp = int(sum(int(i) + 1 for i in rows))
+    allp = c2.n * (c2.n + 1) // 2
+    out.append({"workload": "C2 dense (64 uniform rows, all heads; extrapolated by pair count)",
+                "seconds": dt, "cores": int(used), "mpair_per_s": sp * c2.hq / dt / 1e6,
+                "layer_seconds_extrapolated": dt * allp / sp})
+    return out
 
 
 # ------------------------------------------------------------------ reference arm
@@ -191,12 +289,11 @@ def run_reference(args):
     tot_s = sum(x["seconds"] for x in vals)
     value = tot_fl / tot_s
     line = {
-        "impl": "reference", "metric": "triangle-attn prefill kept-FLOP TFLOP/s (oracle)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / len(vals), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: {c.name} triangle layer si/sl/last="
-                               f"{c.si}/{c.sl}/{c.last}", "seq_len": c.n, "global_batch": 1},
+        "config": config_dict(args, c, args.gpus),
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": vals[0]["cores"],
                          "kind": "oracle", "sample": vals[0]["sample"]},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
@@ -210,6 +307,9 @@ def main():
     args = parse()
     if args.warmup < 3:
         args.warmup = 3
+    spawn_if_needed(args)
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
     import paper_2507_21526_b200 as ta
@@ -249,6 +349,7 @@ def main():
 
     layer = layer_nccl
     gather_mode = "nccl" if world > 1 else None
+    o_result = od   # the buffer holding this rank's O after a step (e2e reads it back)
     if world > 1 and args.gather == "fused":
         # f2: every rank's epilogue stores its O tiles into all ranks' symmetric-memory
         # full-O buffers (own slice + the same head slice of each peer); a device-side
@@ -277,6 +378,7 @@ def main():
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if ok.item() == 1.0:
                 layer, gather_mode = layer_fused, "fused (kernel epilogue -> peer symmetric memory)"
+                o_result = own
             else:
                 gather_mode = "nccl (fused output check failed)"
         except Exception as e:  # no P2P / symmetric memory on this box: report and keep NCCL
@@ -337,7 +439,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         qh, kh, vh = qs.pin_memory(), ks.pin_memory(), vs.pin_memory()
-        oh = torch.empty(qs.shape, dtype=torch.bfloat16).pin_memory()
+        oh = torch.empty(o_result.shape, dtype=torch.bfloat16).pin_memory()
         e_steps = min(args.steps, 3)
 
         def e2e_step():
@@ -345,7 +447,7 @@ def main():
             kd.copy_(kh, non_blocking=True)
             vd.copy_(vh, non_blocking=True)
             layer()
-            oh.copy_(od, non_blocking=True)
+            oh.copy_(o_result, non_blocking=True)
 
         e2e_step()
         barrier()
@@ -362,7 +464,7 @@ def main():
 
     # ---- sweep of the other configs (1 GPU only; extra key)
     sweep = None
-    if args.sweep and world == 1:
+    if not args.no_points and world == 1:
         sweep = []
         for name in ("C2", "C4a", "C4b"):
             cc = synth.CONFIGS[name]
@@ -393,6 +495,38 @@ def main():
             res["workload"] = cc.name
             sweep.append(res)
             del q2, k2, v2, o2
+
+    # ---- strong-scaling proxy on 1 GPU: the per-rank kernel at the 2/4/8-way kv-head
+    # shard shapes of C3 and C2; efficiency = (full-layer ms / P) / shard ms.
+    shard_pts = None
+    if not args.no_points and world == 1:
+        shard_pts = []
+        for name in ("C3", "C2"):
+            cc = synth.CONFIGS[name]
+            full = None
+            for P in (1, 2, 4, 8):
+                g = cc.hq // cc.hkv
+                q1, k1, v1 = (t.to(dev) for t in synth.make_qkv(g * cc.hkv // P, cc.hkv // P, cc.n,
+                                                                   cc.d, seed=100 + P))
+                o1 = torch.empty_like(q1)
+                fn = lambda: ta.triangle_attn_prefill(q1, k1, v1, o1, sink=cc.si, window=cc.sl,
+                                                      last_q=cc.last)
+                for _ in range(3):
+                    fn()
+                barrier()
+                ta.profile_begin()
+                for _ in range(10):
+                    flush.zero_()
+                    fn()
+                barrier()
+                pr = ta.profile_end()
+                kms = (pr["attn_ms"] + pr["merge_ms"]) / 10
+                if P == 1:
+                    full = kms
+                shard_pts.append({"workload": name, "ranks": P, "hq_per_rank": g * cc.hkv // P,
+                                  "kernel_ms_per_rank": kms,
+                                  "strong_scaling_eff": full / (P * kms)})
+                del q1, k1, v1, o1
 
     # ---- NEXT rows on 1 GPU (extra keys): final-layer last rows (f1), StreamingMix (f3),
     # and the C5 attention stack per rank of an 8-way kv-head shard (16 dense + 16 triangle).
@@ -447,25 +581,30 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_run(c, q, k, v, args.cpu_seconds)
         cpu.pop("seconds", None)
+        cpu["extra_points"] = cpu_extra_points(cpu["cores"])
 
     if rank == 0:
         peak, peak_sus, hbm, src = measured_peaks()
         achieved = fl_rank / (attn_ms * 1e-3) / 1e12
+        traffic, traffic_src = ncu_traffic() if (args.workload == "C3" and world == 1) else (None, None)
+        # compulsory bytes of the layer shard: bf16 Q, O (hq_l heads) and K, V (kv heads)
+        hkv_l = plan[rank][1] - plan[rank][0]
+        alg_bytes = 2 * c.n * c.d * (2 * hq_l + 2 * hkv_l)
+        hbm_line = {"algorithmic_bytes_per_launch": alg_bytes,
+                    "algorithmic_gbs": alg_bytes / (attn_ms * 1e-3) / 1e9,
+                    "dram_bytes_per_launch": traffic,
+                    "dram_gbs": (traffic / (attn_ms * 1e-3) / 1e9) if traffic else None,
+                    "peak_gbs": hbm,
+                    "dram_source": traffic_src,
+                    "note": "dram bytes from the ncu --set full capture named in dram_source, "
+                            "divided by this run's CUDA-event kernel time"}
         line = {
-            "metric": "triangle-attn prefill kept-FLOP TFLOP/s (ms/layer, speedup vs dense)",
+            "metric": METRIC,
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_tri, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded iid N(0,1) bf16 Q/K/V, synth recipe)",
-            "config": {"workload": f"{args.workload}: {c.name}, one triangle (deep) layer, "
-                                   f"Hq={c.hq} Hkv={c.hkv} d={c.d} si/sl/last={c.si}/{c.sl}/{c.last}",
-                       "global_batch": 1, "seq_len": c.n,
-                       "parallelism": (f"kv-head shard x{world}" if world <= c.hkv else
-                                       f"q-head split x{world} ({world // c.hkv} ranks per kv head)")
-                                      + (f" + O all-gather: {gather_mode}" if world > 1 else ""),
-                       "l2": ("flushed (512 MiB write) before every timed step; inputs 1.5 GB > L2"
-                              if args.l2 == "flush" else
-                              "no flush: inputs (Q/K/V/O 1.5 GB at C3) exceed the 126 MB L2")},
+            "config": config_dict(args, c, world, gather_mode),
             "ms_per_layer": ms_tri,
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms_tri) if dense_ms else None,
@@ -476,10 +615,11 @@ def main():
             # N > 1: the rest of the step is the O all-gather (NCCL, or the fused f2 barrier)
             "gather_ms": (max(0.0, ms_tri - attn_ms - merge_ms) if world > 1 else None),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
                          "kernel": "attn_kernel<128> (persistent tcgen05 flash attention)",
                          "algorithmic_flops_per_launch": fl_rank},
+            "hbm": hbm_line,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
@@ -488,7 +628,9 @@ def main():
                              "at 32K/64K/128K, P:L433-436; other hardware, context only",
         }
         if sweep is not None:
-            line["sweep"] = sweep
+            line["points"] = sweep
+        if shard_pts is not None:
+            line["shard_points"] = shard_pts
         if extras is not None:
             line["next_rows"] = extras
         print(json.dumps(line), flush=True)

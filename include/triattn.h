@@ -1,4 +1,4 @@
-/* triattn.h -- C ABI v2 of the B200-native TriangleMix prefill-attention library.
+/* triattn.h -- C ABI v4 of the B200-native TriangleMix prefill-attention library.
  *
  * The library computes, for one prefill request (batch 1) and one attention
  * layer, the masked softmax attention of PAPER.md section 2.1
@@ -31,6 +31,8 @@
  *    keyed by device and problem signature, mutex-protected, freed by
  *    ta_release_caches().  Calls from different threads/streams are safe.
  *  - Same inputs + same SM count => bitwise-identical outputs.
+ *  - Kernels run on the calling thread's CURRENT device (cudaGetDevice): every pointer
+ *    and the stream must belong to it (the Python binding sets it from q's device).
  */
 #ifndef TRIATTN_H_
 #define TRIATTN_H_
@@ -42,7 +44,8 @@
 extern "C" {
 #endif
 
-#define TA_ABI_VERSION 3  /* v2: last_q = 0 (StreamingMix), final-layer last-rows entry points; v3: *_multi (f2) */
+#define TA_ABI_VERSION 4  /* v2: last_q = 0 (StreamingMix), final-layer last-rows entry points;
+                             v3: *_multi (f2); v4: ta_set_pdl, PDL-launched merge, multicast f2 */
 
 /* Same type as the CUDA runtime's cudaStream_t (a duplicate identical typedef is
  * legal in C11/C++), so callers need no CUDA headers. NULL = legacy stream. */
@@ -147,6 +150,25 @@ ta_status triangle_attn_prefill_multi(const ta_problem *p, const ta_triangle *tr
 ta_status dense_attn_prefill_multi(const ta_problem *p, const ta_out_tensor *extra_o,
                                    int32_t n_extra, void *ws, size_t ws_bytes, cudaStream_t stream);
 
+/* Multicast variant of f2 (NVLS, SURVEY 8(f) f2 as specified): the kernels additionally
+ * write every finished O tile, and the merged last rows, with 16-byte multimem stores to
+ * mc_o -- a [Hq][N][d] bf16 view (this rank's head slice) inside a buffer mapped at a
+ * MULTICAST virtual address (cuMulticastCreate / cuMulticastBindMem / cuMemMap, or torch
+ * symmetric memory's multicast_ptr) whose physical backing is every rank's full-O buffer.
+ * Each tile leaves this GPU once and the NVSwitch delivers it to every bound GPU
+ * (egress per rank = its O shard, vs (P - 1) x the shard for the unicast *_multi calls).
+ * p->o is written as usual (it may be this rank's unicast view of the same buffer).
+ *   mc_o: device multicast address + element strides; 16-B aligned, strides * 2 multiples
+ *         of 16; caller-owned mapping (the library keeps no pointer past the call).
+ * Visibility on the peers needs a cross-rank barrier after the call (as for *_multi).
+ * Errors: TA_ERR_NULL_ARG (mc_o or its data NULL), TA_ERR_UNSUPPORTED (alignment), as for o.
+ * The plain (non-multimem) store path is unaffected: separate kernel instantiation. */
+ta_status triangle_attn_prefill_multicast(const ta_problem *p, const ta_triangle *tri,
+                                          const ta_out_tensor *mc_o, void *ws, size_t ws_bytes,
+                                          cudaStream_t stream);
+ta_status dense_attn_prefill_multicast(const ta_problem *p, const ta_out_tensor *mc_o, void *ws,
+                                       size_t ws_bytes, cudaStream_t stream);
+
 /* ---- final layer: last query rows only ----------------------- *
  * "For the last layer, only the last r rows of the attention output are needed"
  * (TriangleMix section 2.4): O_last = Softmax(Q_last K^T * scale) V over ALL causal keys
@@ -184,6 +206,12 @@ const char *ta_last_error(void);
 int32_t ta_abi_version(void);
 /* Free library-owned schedule/descriptor caches (device and host). */
 void ta_release_caches(void);
+
+/* Launch the LSE merge kernel with programmatic dependent launch after the
+ * attention kernel (default on): the merge grid's launch overlaps the attention grid's
+ * tail and its griddepcontrol.wait orders every read after the attention grid completes.
+ * on = 0 launches it as a plain stream-ordered kernel.  Returns the previous setting. */
+int32_t ta_set_pdl(int32_t on);
 
 /* ---- kernel timing (used by bench.py) ------------------------------------ */
 /* While enabled, every prefill call records CUDA events on its stream around the

@@ -21,12 +21,14 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 __all__ = [
     "TriattnError", "triangle_attn_prefill", "dense_attn_prefill", "layer_attn_prefill",
     "workspace_size", "pair_count", "schedule_export", "abi_version", "release_caches",
     "triangle_attn_prefill_multi", "dense_attn_prefill_multi",
-    "library_path", "STATUS", "profile_begin", "profile_end", "last_rows_attn_prefill",
+    "triangle_attn_prefill_multicast", "dense_attn_prefill_multicast",
+    "library_path", "STATUS", "profile_begin", "set_pdl", "profile_end", "last_rows_attn_prefill",
     "last_rows_workspace_size", "last_rows_schedule_export",
 ]
 
@@ -88,6 +90,10 @@ def _load():
     lib.triangle_attn_prefill_multi.restype = ctypes.c_int
     lib.dense_attn_prefill_multi.argtypes = [P, vp, ctypes.c_int32, vp, sz, vp]
     lib.dense_attn_prefill_multi.restype = ctypes.c_int
+    lib.triangle_attn_prefill_multicast.argtypes = [P, Tp, ctypes.POINTER(_InTensor), vp, sz, vp]
+    lib.triangle_attn_prefill_multicast.restype = ctypes.c_int
+    lib.dense_attn_prefill_multicast.argtypes = [P, ctypes.POINTER(_InTensor), vp, sz, vp]
+    lib.dense_attn_prefill_multicast.restype = ctypes.c_int
     lib.ta_layer_attn_prefill.argtypes = [ctypes.c_int32, ctypes.c_int32, P, Tp, vp, sz, vp]
     lib.ta_layer_attn_prefill.restype = ctypes.c_int
     lib.ta_pair_count.argtypes = [ctypes.c_int64, Tp, ctypes.POINTER(ctypes.c_int64)]
@@ -108,6 +114,8 @@ def _load():
     lib.ta_abi_version.restype = ctypes.c_int32
     lib.ta_release_caches.argtypes = []
     lib.ta_release_caches.restype = None
+    lib.ta_set_pdl.argtypes = [ctypes.c_int32]
+    lib.ta_set_pdl.restype = ctypes.c_int32
     lib.ta_profile_begin.argtypes = []
     lib.ta_profile_begin.restype = ctypes.c_int
     lib.ta_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
@@ -138,7 +146,7 @@ def _problem(q, k, v, o, lse, scale):
     return p
 
 
-def _check_tensors(q, k, v, o, lse, o_rows=None):
+def _check_tensors(q, k, v, o, lse, o_rows=None, extra=()):
     import torch
     for name, t in (("q", q), ("k", k), ("v", v), ("o", o)):
         if t.dtype != torch.bfloat16 or t.dim() != 3 or not t.is_cuda or t.stride(2) != 1:
@@ -149,12 +157,50 @@ def _check_tensors(q, k, v, o, lse, o_rows=None):
     if lse is not None and (lse.dtype != torch.float32 or not lse.is_contiguous()
                             or tuple(lse.shape) != (q.shape[0], rows)):
         raise TriattnError(3, "lse must be contiguous fp32 [Hq][rows of o]")
+    # one device for every buffer: the library launches on the current device, which the
+    # calls below set to q's (a foreign pointer would fault or silently cross NVLink)
+    for name, t in (("k", k), ("v", v), ("o", o), ("lse", lse)) + tuple(
+            (f"extra_out[{i}]", t) for i, t in enumerate(extra)):
+        if t is not None and t.device != q.device:
+            raise TriattnError(3, f"{name} is on {t.device}, q on {q.device}")
 
 
+class _Call:
+    """Device guard + target stream of one call: the current device is q's for the duration
+    of the C call, and the default stream is the current stream *of q's device*."""
+
+    def __init__(self, device, stream):
+        import torch
+        self.device = device
+        self.guard = torch.cuda.device(device)
+        if stream is None:
+            self.stream = torch.cuda.current_stream(device)
+        elif isinstance(stream, torch.cuda.Stream):
+            self.stream = stream
+        else:  # raw cudaStream_t handle
+            self.stream = torch.cuda.ExternalStream(int(stream), device=device)
+
+    def __enter__(self):
+        self.guard.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        return self.guard.__exit__(*exc)
+
+    @property
+    def handle(self):
+        return self.stream.cuda_stream
+
+
+# Split-K workspace: one buffer per (device, stream), allocated with that stream current so
+# the caching allocator only ever recycles it in that stream's order (calls on different
+# streams never share scratch).  Bounded; an evicted buffer returns to its own stream's pool.
 _ws_cache: dict = {}
+_ws_lock = threading.Lock()
+_WS_MAX_ENTRIES = 8
 
 
-def _workspace(p, tri, device, last_rows=None):
+def _workspace(p, tri, call, last_rows=None):
     import torch
     if last_rows is not None:
         need = _load().ta_last_rows_workspace_size(ctypes.byref(p), int(last_rows))
@@ -162,21 +208,18 @@ def _workspace(p, tri, device, last_rows=None):
         need = _load().ta_workspace_size(ctypes.byref(p), ctypes.byref(tri) if tri is not None else None)
     if need == 0:
         return None, 0
-    key = (device.index, need)
-    buf = _ws_cache.get(key)
-    if buf is None:
-        buf = torch.empty(need + 256, dtype=torch.uint8, device=device)
-        _ws_cache.clear()
-        _ws_cache[key] = buf
+    key = (call.device.index, call.stream.cuda_stream)
+    with _ws_lock:
+        buf = _ws_cache.get(key)
+        if buf is None or buf.numel() < need + 256:
+            with torch.cuda.stream(call.stream):
+                buf = torch.empty(need + 256, dtype=torch.uint8, device=call.device)
+            _ws_cache.pop(key, None)
+            while len(_ws_cache) >= _WS_MAX_ENTRIES:
+                _ws_cache.pop(next(iter(_ws_cache)))
+            _ws_cache[key] = buf
     ptr = (buf.data_ptr() + 255) // 256 * 256
     return ptr, need
-
-
-def _stream(stream):
-    import torch
-    if stream is None:
-        return torch.cuda.current_stream().cuda_stream
-    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
 def triangle_attn_prefill(q, k, v, o=None, *, sink: int = 8, window: int = 512, last_q: int = 128,
@@ -188,9 +231,9 @@ def triangle_attn_prefill(q, k, v, o=None, *, sink: int = 8, window: int = 512, 
     _check_tensors(q, k, v, o, lse)
     p = _problem(q, k, v, o, lse, scale)
     tri = _Triangle(sink, window, last_q)
-    ws, need = _workspace(p, tri, q.device)
-    _check(_load().triangle_attn_prefill(ctypes.byref(p), ctypes.byref(tri), ws, need,
-                                         _stream(stream)))
+    with _Call(q.device, stream) as c:
+        ws, need = _workspace(p, tri, c)
+        _check(_load().triangle_attn_prefill(ctypes.byref(p), ctypes.byref(tri), ws, need, c.handle))
     return o
 
 
@@ -214,13 +257,14 @@ def triangle_attn_prefill_multi(q, k, v, extra_out, o=None, *, sink: int = 8, wi
     import torch
     if o is None:
         o = torch.empty_like(q)
-    _check_tensors(q, k, v, o, lse)
+    _check_tensors(q, k, v, o, lse, extra=tuple(extra_out))
     arr, n = _extra_views(extra_out, o)
     p = _problem(q, k, v, o, lse, scale)
     tri = _Triangle(sink, window, last_q)
-    ws, need = _workspace(p, tri, q.device)
-    _check(_load().triangle_attn_prefill_multi(ctypes.byref(p), ctypes.byref(tri), arr, n, ws, need,
-                                               _stream(stream)))
+    with _Call(q.device, stream) as c:
+        ws, need = _workspace(p, tri, c)
+        _check(_load().triangle_attn_prefill_multi(ctypes.byref(p), ctypes.byref(tri), arr, n, ws,
+                                                   need, c.handle))
     return o
 
 
@@ -230,11 +274,55 @@ def dense_attn_prefill_multi(q, k, v, extra_out, o=None, *, lse=None, scale: flo
     import torch
     if o is None:
         o = torch.empty_like(q)
-    _check_tensors(q, k, v, o, lse)
+    _check_tensors(q, k, v, o, lse, extra=tuple(extra_out))
     arr, n = _extra_views(extra_out, o)
     p = _problem(q, k, v, o, lse, scale)
-    ws, need = _workspace(p, None, q.device)
-    _check(_load().dense_attn_prefill_multi(ctypes.byref(p), arr, n, ws, need, _stream(stream)))
+    with _Call(q.device, stream) as c:
+        ws, need = _workspace(p, None, c)
+        _check(_load().dense_attn_prefill_multi(ctypes.byref(p), arr, n, ws, need, c.handle))
+    return o
+
+
+def _mc_view(mc_ptr, mc_strides):
+    if not mc_ptr:
+        raise TriattnError(1, "multicast pointer is NULL")
+    sh, st = mc_strides
+    return _InTensor(int(mc_ptr), int(sh), int(st))
+
+
+def triangle_attn_prefill_multicast(q, k, v, mc_ptr: int, mc_strides, o=None, *, sink: int = 8,
+                                    window: int = 512, last_q: int = 128, lse=None,
+                                    scale: float = 0.0, stream=None):
+    """triangle_attn_prefill that also stores every O tile (and the merged last rows) with
+    multimem stores to a [Hq][N][d] view at the multicast address mc_ptr (element strides
+    mc_strides = (stride_head, stride_token)): f2 over NVLS, one egress per tile."""
+    import torch
+    if o is None:
+        o = torch.empty_like(q)
+    _check_tensors(q, k, v, o, lse)
+    mc = _mc_view(mc_ptr, mc_strides)
+    p = _problem(q, k, v, o, lse, scale)
+    tri = _Triangle(sink, window, last_q)
+    with _Call(q.device, stream) as c:
+        ws, need = _workspace(p, tri, c)
+        _check(_load().triangle_attn_prefill_multicast(ctypes.byref(p), ctypes.byref(tri),
+                                                       ctypes.byref(mc), ws, need, c.handle))
+    return o
+
+
+def dense_attn_prefill_multicast(q, k, v, mc_ptr: int, mc_strides, o=None, *, lse=None,
+                                 scale: float = 0.0, stream=None):
+    """dense_attn_prefill with the f2 multicast output view; returns o."""
+    import torch
+    if o is None:
+        o = torch.empty_like(q)
+    _check_tensors(q, k, v, o, lse)
+    mc = _mc_view(mc_ptr, mc_strides)
+    p = _problem(q, k, v, o, lse, scale)
+    with _Call(q.device, stream) as c:
+        ws, need = _workspace(p, None, c)
+        _check(_load().dense_attn_prefill_multicast(ctypes.byref(p), ctypes.byref(mc), ws, need,
+                                                    c.handle))
     return o
 
 
@@ -245,8 +333,9 @@ def dense_attn_prefill(q, k, v, o=None, *, lse=None, scale: float = 0.0, stream=
         o = torch.empty_like(q)
     _check_tensors(q, k, v, o, lse)
     p = _problem(q, k, v, o, lse, scale)
-    ws, need = _workspace(p, None, q.device)
-    _check(_load().dense_attn_prefill(ctypes.byref(p), ws, need, _stream(stream)))
+    with _Call(q.device, stream) as c:
+        ws, need = _workspace(p, None, c)
+        _check(_load().dense_attn_prefill(ctypes.byref(p), ws, need, c.handle))
     return o
 
 
@@ -260,9 +349,10 @@ def layer_attn_prefill(layer: int, tri_start: int, q, k, v, o=None, *, sink: int
     _check_tensors(q, k, v, o, lse)
     p = _problem(q, k, v, o, lse, scale)
     tri = _Triangle(sink, window, last_q)
-    ws, need = _workspace(p, None if layer < tri_start else tri, q.device)
-    _check(_load().ta_layer_attn_prefill(layer, tri_start, ctypes.byref(p), ctypes.byref(tri), ws,
-                                         need, _stream(stream)))
+    with _Call(q.device, stream) as c:
+        ws, need = _workspace(p, None if layer < tri_start else tri, c)
+        _check(_load().ta_layer_attn_prefill(layer, tri_start, ctypes.byref(p), ctypes.byref(tri), ws,
+                                             need, c.handle))
     return o
 
 
@@ -276,8 +366,9 @@ def last_rows_attn_prefill(q, k, v, o=None, *, last_q: int = 128, lse=None, scal
         o = torch.empty((q.shape[0], max(r, 0), q.shape[2]), dtype=q.dtype, device=q.device)
     _check_tensors(q, k, v, o, lse, o_rows=max(r, 0))
     p = _problem(q, k, v, o, lse, scale)
-    ws, need = _workspace(p, None, q.device, last_rows=last_q)
-    _check(_load().last_rows_attn_prefill(ctypes.byref(p), int(last_q), ws, need, _stream(stream)))
+    with _Call(q.device, stream) as c:
+        ws, need = _workspace(p, None, c, last_rows=last_q)
+        _check(_load().last_rows_attn_prefill(ctypes.byref(p), int(last_q), ws, need, c.handle))
     return o
 
 
@@ -340,6 +431,12 @@ def abi_version() -> int:
 
 def release_caches() -> None:
     _load().ta_release_caches()
+
+
+def set_pdl(on: bool) -> bool:
+    """Launch the LSE merge with programmatic dependent launch (default on); returns the
+    previous setting."""
+    return bool(_load().ta_set_pdl(1 if on else 0))
 
 
 def profile_begin() -> None:

@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtriattn.so")
 SO_TRACE = os.path.join(HERE, "libtriattn_trace.so")
+SO_COUNT = os.path.join(HERE, "libtriattn_count.so")  # TA_COUNT: per-row pair counters
 SOURCES = ["api.cu", "kernels.cu", "schedule.cpp"]
 HEADERS = ["ptx.cuh", "kernel_params.h", "schedule.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -29,6 +30,24 @@ def _stale() -> bool:
     deps.append(os.path.join(os.path.dirname(HERE), "include", "triattn.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _stale_so(so: str) -> bool:
+    if not os.path.exists(so):
+        return True
+    t = os.path.getmtime(so)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(os.path.dirname(HERE), "include", "triattn.h"))
+    deps.append(os.path.abspath(__file__))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_count(force: bool = False) -> str:
+    """The TA_COUNT build (libtriattn_count.so): same kernels, plus per-row counters of the
+    admitted pairs and computed S columns (GPU-side kept-work proof, tests/test_gpu_count.py)."""
+    if not force and not _stale_so(SO_COUNT):
+        return SO_COUNT
+    return build(force=True, defines=("TA_COUNT",), out=SO_COUNT)
 
 
 def build(force: bool = False, verbose: bool = False, trace: bool = False, defines=(),
@@ -55,3 +74,5 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, defin
 
 if __name__ == "__main__":
     print(build(force=True, verbose="--verbose" in sys.argv, trace="--trace" in sys.argv))
+    if "--trace" not in sys.argv:
+        print(build_count(force=True))

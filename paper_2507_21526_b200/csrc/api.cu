@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -186,9 +187,12 @@ ta_status encode_map(CUtensorMap *m, const void *data, int64_t n, int heads, int
   return TA_OK;
 }
 
-#if defined(TA_TRACE) || defined(TA_CTA_CLOCK)
+#if defined(TA_TRACE) || defined(TA_CTA_CLOCK) || defined(TA_COUNT)
 unsigned long long *g_trace_buf = nullptr;
+size_t g_trace_bytes = sizeof(unsigned long long) * 65536 * 8;
 #endif
+
+std::atomic<int> g_pdl{1};  // merge launched with programmatic dependent launch
 
 // ------------------------------------------------------------------ timing
 struct Timing {
@@ -226,7 +230,7 @@ bool call_geometry(const ta_problem *p, const ta_triangle *tri, Mode mode, int32
 
 ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t last_q, void *ws,
               size_t ws_bytes, cudaStream_t stream, const ta_out_tensor *extra_o = nullptr,
-              int32_t n_extra = 0) {
+              int32_t n_extra = 0, const ta_out_tensor *mc_o = nullptr) {
   const bool dense = mode == kDenseMode;
   ta_status s = validate_shape(p);
   if (s != TA_OK) return s;
@@ -243,6 +247,9 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
     if ((s = validate_tensor("extra_o", extra_o[e].data, extra_o[e].stride_head,
                              extra_o[e].stride_token, p->num_q_heads, o_rows, p->head_dim)))
       return s;
+  if (mc_o && (s = validate_tensor("mc_o", mc_o->data, mc_o->stride_head, mc_o->stride_token,
+                                   p->num_q_heads, o_rows, p->head_dim)))
+    return s;
   int dev;
   DeviceInfo di;
   if ((s = device_info(&dev, &di)) != TA_OK) return s;
@@ -296,6 +303,11 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
     prm.ox_sh[e] = extra_o[e].stride_head;
     prm.ox_st[e] = extra_o[e].stride_token;
   }
+  if (mc_o) {
+    prm.mc_o = mc_o->data;
+    prm.mc_sh = mc_o->stride_head;
+    prm.mc_st = mc_o->stride_token;
+  }
   prm.lse = p->lse;
   if (need > 0) {
     const int64_t slots = ta::num_partial_slots(ds.g);
@@ -340,6 +352,22 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
     g_trace_buf = cbuf;
   }
 #endif
+#if defined(TA_COUNT)
+  {  // per-(q head, token) counters {admitted pairs, computed S columns} (u32 pairs)
+    static unsigned long long *kbuf = nullptr;
+    static size_t kcap = 0;
+    const size_t need = sizeof(uint32_t) * 2 * (size_t)g.hq * (size_t)g.n;
+    if (need > kcap) {
+      if (kbuf) cudaFree(kbuf);
+      if (cudaMalloc(&kbuf, need) != cudaSuccess) return fail(TA_ERR_CUDA, "count buffer");
+      kcap = need;
+    }
+    cudaMemsetAsync(kbuf, 0, need, stream);
+    prm.trace = kbuf;
+    g_trace_buf = kbuf;
+    g_trace_bytes = need;
+  }
+#endif
 #ifdef TA_TRACE
   {
     static unsigned long long *tbuf = nullptr;
@@ -355,7 +383,7 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
   if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
   if (rec.a1) cudaEventRecord(rec.a1, stream);
   if (!dense && ds.g.n_last_pairs > 0) {
-    e = ta::launch_merge(prm, g.d, g.hkv, stream);
+    e = ta::launch_merge(prm, g.d, g.hkv, stream, g_pdl.load(std::memory_order_relaxed) != 0);
     if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
     if (rec.a0) {
       rec.m1 = take_event();
@@ -414,6 +442,32 @@ ta_status triangle_attn_prefill_multi(const ta_problem *p, const ta_triangle *tr
   try {
     if (!tri) return fail(TA_ERR_NULL_ARG, "triangle parameters are NULL");
     return run(p, tri, kTriangle, 0, ws, ws_bytes, stream, extra_o, n_extra);
+  } catch (const std::exception &ex) {
+    return fail(TA_ERR_CUDA, ex.what());
+  } catch (...) {
+    return fail(TA_ERR_CUDA, "unknown exception");
+  }
+}
+
+ta_status triangle_attn_prefill_multicast(const ta_problem *p, const ta_triangle *tri,
+                                          const ta_out_tensor *mc_o, void *ws, size_t ws_bytes,
+                                          cudaStream_t stream) {
+  try {
+    if (!tri) return fail(TA_ERR_NULL_ARG, "triangle parameters are NULL");
+    if (!mc_o) return fail(TA_ERR_NULL_ARG, "mc_o is NULL");
+    return run(p, tri, kTriangle, 0, ws, ws_bytes, stream, nullptr, 0, mc_o);
+  } catch (const std::exception &ex) {
+    return fail(TA_ERR_CUDA, ex.what());
+  } catch (...) {
+    return fail(TA_ERR_CUDA, "unknown exception");
+  }
+}
+
+ta_status dense_attn_prefill_multicast(const ta_problem *p, const ta_out_tensor *mc_o, void *ws,
+                                       size_t ws_bytes, cudaStream_t stream) {
+  try {
+    if (!mc_o) return fail(TA_ERR_NULL_ARG, "mc_o is NULL");
+    return run(p, nullptr, kDenseMode, 0, ws, ws_bytes, stream, nullptr, 0, mc_o);
   } catch (const std::exception &ex) {
     return fail(TA_ERR_CUDA, ex.what());
   } catch (...) {
@@ -583,15 +637,21 @@ ta_status ta_profile_end(double *attn_ms, int64_t *attn_launches, double *merge_
   return st;
 }
 
-#if defined(TA_TRACE) || defined(TA_CTA_CLOCK)
-/* Debug build only: copy the last launch's timeline (4 x 65536 u64) to the host. */
+#if defined(TA_TRACE) || defined(TA_CTA_CLOCK) || defined(TA_COUNT)
+/* Debug builds only: copy the last launch's timeline (TA_TRACE), per-CTA cycle counts
+   (TA_CTA_CLOCK) or per-row pair counters (TA_COUNT: u32 {admitted, computed} per
+   [q head][token]) to the host.  Synchronises the device. */
 ta_status ta_debug_trace_read(void *host, size_t cap) {
   if (!g_trace_buf) return TA_ERR_CUDA;
-  size_t n = sizeof(unsigned long long) * 65536 * 8;
+  const size_t n = g_trace_bytes;
   cudaMemcpy(host, g_trace_buf, cap < n ? cap : n, cudaMemcpyDeviceToHost);
   return TA_OK;
 }
 #endif
+
+int32_t ta_set_pdl(int32_t on) {
+  return g_pdl.exchange(on ? 1 : 0);
+}
 
 void ta_release_caches(void) {
   std::lock_guard<std::mutex> lk(g_mu);

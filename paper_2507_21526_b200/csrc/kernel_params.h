@@ -43,11 +43,15 @@ struct alignas(64) AttnParams {
   void *ox[kMaxExtraOut];
   int64_t ox_sh[kMaxExtraOut], ox_st[kMaxExtraOut];
   CUtensorMap tm_ox[kMaxExtraOut];
+  // f2 multicast: the same O view at a multicast virtual address (NVLS: one store reaches
+  // every GPU bound to the multicast object); NULL = none.  Element strides as for o.
+  void *mc_o;
+  int64_t mc_sh, mc_st;
 };
 
 // Launchers (kernels.cu). Return the CUDA error of the launch.
 cudaError_t launch_attention(const AttnParams &p, int head_dim, int num_ctas, cudaStream_t s);
-cudaError_t launch_merge(const AttnParams &p, int head_dim, int hkv, cudaStream_t s);
+cudaError_t launch_merge(const AttnParams &p, int head_dim, int hkv, cudaStream_t s, bool pdl);
 size_t attention_smem_bytes(int head_dim);
 
 }  // namespace ta

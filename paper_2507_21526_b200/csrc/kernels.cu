@@ -28,6 +28,8 @@
 // start of the sliding-window band.
 #include <cuda_bf16.h>
 
+#include <atomic>
+
 #include "kernel_params.h"
 #include "ptx.cuh"
 
@@ -125,8 +127,17 @@ constexpr int kEmpty = 1 << 30;            // canonical empty column interval [k
 // instead of MUFU.EX2.  Default 0: every exponential on MUFU -- with the exp phase bound by
 // the FMA pipe (FFMA2 scale, FADD2 row sum, F2FP) the offload measured slower (cycles per
 // item: 0x25 +2.4 %, 0x11 +2.2 %, 0x01 +0.5 % vs 0x00; scripts/variant_cycles.py).
+// Row sum l (the softmax denominator): 4 (default) = the bf16-rounded P that the PV MMA
+// consumes, added with mixed-precision FHADD.BF16 (exact normalisation: V = 1 gives O = 1,
+// and a row dominated by one key carries no P-rounding mismatch between O and l; +3.1 %
+// cycles at C3 vs the fp32 sum).  0 = fp32 p (FADD2); 1 / 2 = unpack the bf16 pair
+// (IMAD.SHL + LOP3 / PRMT + LOP3) + FADD2 (+9 % / +10 %); 3 = truncate P on the ALU pipe
+// (+7.6 %).  Measured with scripts/variant_ctaclk.py.
 #ifndef TA_SUM_ROUNDED
-#define TA_SUM_ROUNDED 0
+#define TA_SUM_ROUNDED 4
+#endif
+#ifndef TA_FHADD_ACC  // independent FHADD accumulators per row (2: -0.5 % cycles vs 4)
+#define TA_FHADD_ACC 2
 #endif
 #ifndef TA_SM_WAIT
 #define TA_SM_WAIT 0
@@ -341,6 +352,32 @@ __device__ __forceinline__ uint64_t u2pack(uint32_t lo, uint32_t hi) {
   return r;
 }
 
+#if TA_SUM_ROUNDED == 2 || TA_SUM_ROUNDED == 3
+// bf16 bit helpers pinned to the integer ALU pipe (the compiler would otherwise emit
+// IMAD.SHL on the FMA pipe, which the exponential phase already saturates).
+__device__ __forceinline__ uint32_t hi16(uint32_t a) {  // a & 0xffff0000 (LOP3)
+  uint32_t r;
+  asm("and.b32 %0, %1, 0xffff0000;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t lo16_up(uint32_t a) {  // a << 16 (PRMT)
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t prmt_hi(uint32_t lo, uint32_t hi) {  // {hi.hi16, lo.hi16}
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+#endif
+__device__ __forceinline__ void sum_bf16_lo(float &acc, uint32_t pk) {
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.bf16 %0, l, %0;\n\t}" : "+f"(acc) : "r"(pk));
+}
+__device__ __forceinline__ void sum_bf16_hi(float &acc, uint32_t pk) {
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.bf16 %0, h, %0;\n\t}" : "+f"(acc) : "r"(pk));
+}
+
 // Bits [lo, hi] of a 32-bit word (empty if hi < lo or outside [0, 31]).
 __device__ __forceinline__ uint32_t iv_bits(int lo, int hi) {
   lo = max(lo, 0);
@@ -380,10 +417,23 @@ __device__ __forceinline__ void norm_iv(int &lo, int &hi) {
   }
 }
 
-// kMulti: the f2 entry points (extra output destinations, p.n_ox > 0) get their own
-// instantiation, so the single-output epilogue -- on the kernel's critical path -- carries
-// no destination loop (it measured +2.5 % cycles when shared).
-template <int D, bool kMulti>
+// 16-byte store to a multicast (NVLS) address: one egress, every bound GPU receives it.
+__device__ __forceinline__ void mc_st16(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("multimem.st.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void mc_st4(void *p, uint32_t a) {
+  asm volatile("multimem.st.global.bf16x2 [%0], %1;" ::"l"(p), "r"(a) : "memory");
+}
+
+// Output modes.  The f2 entry points get their own instantiations, so the single-output
+// epilogue -- on the kernel's critical path -- carries no destination code (a destination
+// loop compiled into it measured +2.5 % cycles).
+constexpr int kOutSingle = 0;     // TMA store to p.o
+constexpr int kOutExtra = 1;      // + TMA stores to up to 7 extra destinations (unicast)
+constexpr int kOutMulticast = 2;  // + 16-byte multimem stores to the multicast view p.mc_o
+template <int D, int kMode>
 __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant__ AttnParams p) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -759,6 +809,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       const bool last_row = tok >= p.n - p.last;
       float m_run = -INFINITY;  // reference max, log2 units of scaled scores
       float l_run = 0.f;        // running sum of 2^(x - m_run) over this thread's columns
+#ifdef TA_COUNT
+      uint32_t n_adm = 0, n_cmp = 0;
+#endif
       for (int j = 0; j < f.nb; ++j) {
         const Blk b = block_info(f, j);
         // Kept columns of row i in this block: [a_lo, a_hi] U [b_lo, b_hi]   (reading R1)
@@ -801,6 +854,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         a_hi -= c0;
         norm_iv(a_lo, a_hi);
         norm_iv(b_lo, b_hi);
+#ifdef TA_COUNT
+        {  // admitted keys of this row in the block (its kept-column intervals within the
+           // computed columns) and the S columns the MMA computed for it
+          const int lim = tile_ncols(f, b, x, T) - 1 - c0;
+          auto span = [&](int lo, int hi) { lo = max(lo, 0); hi = min(hi, lim); return hi >= lo ? hi - lo + 1 : 0; };
+          n_adm += span(a_lo, a_hi) + span(b_lo, b_hi);
+          n_cmp += tile_ncols(f, b, x, T);
+        }
+#endif
         // All kNCol columns are processed every block (columns >= ncols are masked): no
         // data-dependent branches inside the row loop.
         constexpr int L = kNCol - 1;
@@ -895,7 +957,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         spin_cycles(TA_DELAY_SM);
         const uint64_t sc2 = f2pack(sc, sc);
         uint64_t nref2 = f2pack(-ref, -ref);
+#if TA_SUM_ROUNDED == 4
+        float lsa = 0.f, lsb = 0.f, lsc = 0.f, lsd = 0.f;  // FHADD partial row sums
+#else
         uint64_t l2a = 0, l2b = 0;  // packed partial row sums (FADD2)
+#endif
         uint32_t pkw[16];           // bf16 P pairs of one (TA_TMEM_WIDE: two) 16-key chunks
 #pragma unroll
         for (int c = 0; c < kNCol / 16; ++c) {
@@ -921,17 +987,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
               p0 = ptx::ex2(x0);            // MUFU
               p1 = ptx::ex2(x1);
             }
+#if TA_SUM_ROUNDED == 3
+            // P truncated to bf16 on the ALU pipe (LOP3 x2 + PRMT instead of F2FP); the row
+            // sum adds exactly the values the PV MMA consumes (exact normalisation).
+            const uint32_t t0 = hi16(__float_as_uint(p0)), t1 = hi16(__float_as_uint(p1));
+            pk[e / 2] = prmt_hi(__float_as_uint(p0), __float_as_uint(p1));
+            const uint64_t pr = u2pack(t0, t1);
+#elif TA_SUM_ROUNDED == 4
             pk[e / 2] = ptx::pack_bf16(p0, p1);
-#if TA_SUM_ROUNDED
+            // mixed-precision adds (FHADD.BF16) of the two rounded halves
+#if TA_FHADD_ACC == 2
+            sum_bf16_lo(lsa, pk[e / 2]);
+            sum_bf16_hi(lsb, pk[e / 2]);
+#else
+            if (e & 2) {
+              sum_bf16_lo(lsa, pk[e / 2]);
+              sum_bf16_hi(lsb, pk[e / 2]);
+            } else {
+              sum_bf16_lo(lsc, pk[e / 2]);
+              sum_bf16_hi(lsd, pk[e / 2]);
+            }
+#endif
+#else
+            pk[e / 2] = ptx::pack_bf16(p0, p1);
+#if TA_SUM_ROUNDED == 1
             // row sum of the bf16-rounded P the PV MMA actually uses (exact normalisation)
             const uint64_t pr = u2pack(pk[e / 2] << 16, pk[e / 2] & 0xffff0000u);
+#elif TA_SUM_ROUNDED == 2
+            // the same with both unpacks forced onto the ALU pipe (PRMT + LOP3)
+            const uint64_t pr = u2pack(lo16_up(pk[e / 2]), hi16(pk[e / 2]));
 #else
             const uint64_t pr = f2pack(p0, p1);
 #endif
+#endif
+#if TA_SUM_ROUNDED != 4
             if (e & 2)
               l2b = fadd2(l2b, pr);
             else
               l2a = fadd2(l2a, pr);
+#endif
           }
           if (!TA_TMEM_WIDE)
             ptx::tmem_st8(tS + c * 8, pk);
@@ -957,10 +1051,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ++ecount;
         TRACE_SM(26, j);
         {
+#if TA_SUM_ROUNDED == 4
+          l_run += (lsa + lsb) + (lsc + lsd);
+#else
           const uint64_t l2 = fadd2(l2a, l2b);
           float a0, a1;
           f2unpack(l2, a0, a1);
           l_run += a0 + a1;
+#endif
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
@@ -979,6 +1077,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         if (hc == 0) sts_f32(ptx::smem_u32(red_m + (par * 2 + x) * kTileRows + r), m_run);
         sm_arrive(&l_ready[x]);
         ++kitem_sm;
+#ifdef TA_COUNT
+        if (row_in_tile && tok < p.n) {
+          uint32_t *cnt = reinterpret_cast<uint32_t *>(p.trace) +
+                          2 * ((int64_t)(f.kvh * p.group + r / T) * p.n + tok);
+          atomicAdd(cnt, n_adm);
+          atomicAdd(cnt + 1, n_cmp);
+        }
+#endif
       }
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
@@ -1064,10 +1170,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             if (threadIdx.x == kEpiWarp0 * 32) {
               ptx::tma_store_3d(&p.tm_o, stage, hb * 64, f.r0 + x * T, f.kvh * p.group);
               // f2: the same staged tile to every extra destination (peer ranks' O)
-              if (kMulti)
+              if (kMode == kOutExtra)
                 for (int e = 0; e < p.n_ox; ++e)
                   ptx::tma_store_3d(&p.tm_ox[e], stage, hb * 64, f.r0 + x * T, f.kvh * p.group);
               ptx::bulk_commit();
+            }
+            if (kMode == kOutMulticast) {
+              // f2 multicast: the staged half tile (128 rows x 128 B, 128B-swizzled) to the
+              // multicast view, 16 B per lane, 8 lanes per contiguous row segment.
+              const int pc = (threadIdx.x - kEpiWarp0 * 32) & 7;
+#pragma unroll 1
+              for (int rr = (threadIdx.x - kEpiWarp0 * 32) >> 3; rr < kTileRows; rr += 16) {
+                const int tk = f.r0 + x * T + rr % T;
+                if (rr < p.group * T && tk < p.n) {
+                  uint32_t w0, w1, w2, w3;
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                               : "r"(stage_s + rr * 128 + ((pc ^ (rr & 7)) << 4)));
+                  __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(p.mc_o) +
+                                       (int64_t)(f.kvh * p.group + rr / T) * p.mc_sh + (int64_t)tk * p.mc_st +
+                                       hb * 64 + pc * 8;
+                  mc_st16(dst, w0, w1, w2, w3);
+                }
+              }
             }
             TRACE_EP(44 + hb, kitem);
           }
@@ -1083,6 +1208,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   }
   if (threadIdx.x == kEpiWarp0 * 32) ptx::bulk_wait0();  // epilogue TMA stores complete
   __syncthreads();
+  // PDL: this CTA's work is issued; the merge grid may begin launching (its
+  // griddepcontrol.wait still orders every read after this grid's completion).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef TA_CTA_CLOCK
   if (threadIdx.x == 0) p.trace[blockIdx.x] = (unsigned long long)(clock64() - cta_t0);
 #endif
@@ -1092,52 +1220,69 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   }
 }
 
-// One warp per packed row of a last pair: O = sum_c e^{LSE_c - M} O_c / sum_c e^{LSE_c - M}
-// over the pair's split-K chunks (merge_output; reading R8/R18).
-template <int D>
+// LSE merge of the split-K partials of the last pairs (merge_output; readings
+// R8/R18): per packed row, O = sum_c e^{LSE_c - M} O_c / sum_c e^{LSE_c - M} over the pair's
+// chunks c, M = max_c LSE_c; a chunk with LSE = -inf has weight 0.  W warps share a row
+// (chunks strided over the warps; W grows with the chunk count so that rows with many
+// chunks -- small head shards, where ck is small -- still spread over the whole GPU),
+// combined through shared memory.  Launched with PDL (griddepcontrol.wait first).
+template <int D, int W>
 __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ AttnParams p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr int E = D / 32;
+  constexpr int RPB = 8 / W;  // rows per block
+  __shared__ float s_max[8], s_w[8];
+  __shared__ float s_acc[8][D];  // [warp][32 e + lane]: element pair order of the lane
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t gw = (int64_t)blockIdx.x * 8 + warp;  // (kvh, last pair, row) linear
+  const int sub = warp % W, rib = warp / W;
   const int rows = 2 * kTileRows;
+  const int64_t gr = (int64_t)blockIdx.x * RPB + rib;  // (kvh, last pair, packed row) linear
   const int64_t per_kvh = (int64_t)p.n_last_pairs * rows;
-  const int kvh = (int)(gw / per_kvh);
-  const int rem = (int)(gw % per_kvh);
+  const int kvh = (int)(gr / per_kvh);
+  const int rem = (int)(gr % per_kvh);
   const int lp = rem / rows, rr = rem % rows;
-  if (kvh >= p.hq / p.group) return;
   const int x = rr / kTileRows, r = rr % kTileRows;
   const int T = p.tile_tokens;
-  if (r >= p.group * T) return;
   const int pair = p.p_last0 + lp;
   const int tok = pair * p.pair_tokens + x * T + r % T;
-  if (tok >= p.n) return;
-  if (p.last_only && tok < p.n - p.last) return;  // final-layer mode: last rows only
-  const int head = kvh * p.group + r / T;
+  // rows without output still take part in the block barriers
+  bool live = kvh < p.hq / p.group && r < p.group * T && tok < p.n &&
+              !(p.last_only && tok < p.n - p.last);
   const int r1 = min((pair + 1) * p.pair_tokens, p.n) - 1;
-  const int nch = (r1 + 1 + p.chunk_keys - 1) / p.chunk_keys;
+  const int nch = live ? (r1 + 1 + p.chunk_keys - 1) / p.chunk_keys : 0;
   const int64_t slot0 = ((int64_t)kvh * p.n_last_pairs + lp) * p.s_max;
   float mx = -INFINITY;
-  for (int c = lane; c < nch; c += 32) mx = fmaxf(mx, p.part_lse[(slot0 + c) * rows + rr]);
+  for (int c = sub + W * lane; c < nch; c += 32 * W) mx = fmaxf(mx, p.part_lse[(slot0 + c) * rows + rr]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  constexpr int E = D / 32;
+  if (W > 1) {
+    if (lane == 0) s_max[warp] = mx;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < W; ++w) mx = fmaxf(mx, s_max[rib * W + w]);
+  }
+  // lane owns the element pairs (2 lane + 64 q, 2 lane + 64 q + 1), q < E / 2
   float acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   float wsum = 0.f;
-  // Four chunks per step with all their loads issued first (the merge is latency-bound:
-  // one warp per row, fewer warps than the GPU holds).
+  // Four chunks per step with all their loads issued first (latency-bound loop).
   constexpr int U = 4;
-  for (int c0 = 0; c0 < nch; c0 += U) {
+  for (int c0 = sub; c0 < nch; c0 += U * W) {
     float lcs[U], vv[U][E];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int c = c0 + u;
+      const int c = c0 + u * W;
       lcs[u] = -INFINITY;
       if (c < nch) {
         lcs[u] = p.part_lse[(slot0 + c) * rows + rr];
-        const float *src = p.part_o + ((slot0 + c) * rows + rr) * D;
+        const float2 *src = reinterpret_cast<const float2 *>(p.part_o + ((slot0 + c) * rows + rr) * D);
 #pragma unroll
-        for (int e = 0; e < E; ++e) vv[u][e] = src[lane + 32 * e];
+        for (int q = 0; q < E / 2; ++q) {
+          const float2 t = src[lane + 32 * q];
+          vv[u][2 * q] = t.x;
+          vv[u][2 * q + 1] = t.y;
+        }
       }
     }
 #pragma unroll
@@ -1149,17 +1294,44 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Attn
       for (int e = 0; e < E; ++e) acc[e] += w * vv[u][e];
     }
   }
+  if (W > 1) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) s_acc[warp][32 * e + lane] = acc[e];
+    if (lane == 0) s_w[warp] = wsum;
+    __syncthreads();
+    if (sub != 0) return;
+    wsum = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      wsum += s_w[rib * W + w];
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] += s_acc[rib * W + w][32 * e + lane];
+    }
+  }
+  if (!live) return;
+  const int head = kvh * p.group + r / T;
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
   const int orow = tok - p.o_row0;
-  __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(p.o) + (int64_t)head * p.o_sh +
-                       (int64_t)orow * p.o_st;
+  uint32_t ov[E / 2];
 #pragma unroll
-  for (int e = 0; e < E; ++e) dst[lane + 32 * e] = __float2bfloat16_rn(acc[e] * inv);
+  for (int q = 0; q < E / 2; ++q) ov[q] = ptx::pack_bf16(acc[2 * q] * inv, acc[2 * q + 1] * inv);
+  uint32_t *dst = reinterpret_cast<uint32_t *>(reinterpret_cast<__nv_bfloat16 *>(p.o) +
+                                               (int64_t)head * p.o_sh + (int64_t)orow * p.o_st);
+#pragma unroll
+  for (int q = 0; q < E / 2; ++q) dst[lane + 32 * q] = ov[q];
   for (int x2 = 0; x2 < p.n_ox; ++x2) {  // f2: extra destinations
-    __nv_bfloat16 *d2 = reinterpret_cast<__nv_bfloat16 *>(p.ox[x2]) + (int64_t)head * p.ox_sh[x2] +
-                        (int64_t)orow * p.ox_st[x2];
+    uint32_t *d2 = reinterpret_cast<uint32_t *>(reinterpret_cast<__nv_bfloat16 *>(p.ox[x2]) +
+                                                (int64_t)head * p.ox_sh[x2] + (int64_t)orow * p.ox_st[x2]);
 #pragma unroll
-    for (int e = 0; e < E; ++e) d2[lane + 32 * e] = __float2bfloat16_rn(acc[e] * inv);
+    for (int q = 0; q < E / 2; ++q) d2[lane + 32 * q] = ov[q];
+  }
+  if (p.mc_o) {  // f2 multicast view
+    uint32_t *d2 = reinterpret_cast<uint32_t *>(reinterpret_cast<__nv_bfloat16 *>(p.mc_o) +
+                                                (int64_t)head * p.mc_sh + (int64_t)orow * p.mc_st);
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q) mc_st4(d2 + lane + 32 * q, ov[q]);
   }
   if (lane == 0 && p.lse)
     p.lse[(int64_t)head * (p.n - p.o_row0) + orow] = wsum > 0.f ? mx + __logf(wsum) : -INFINITY;
@@ -1171,36 +1343,64 @@ size_t attention_smem_bytes(int head_dim) {
   return head_dim == 128 ? Cfg<128>::kSmem : Cfg<64>::kSmem;
 }
 
-template <int D, bool M>
+template <int D, int M>
 static cudaError_t launch_attention_t(const AttnParams &p, int num_ctas, cudaStream_t s) {
-  static bool attr_set = false;  // per-process; cudaFuncSetAttribute is cheap and idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_kernel<D, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg<D>::kSmem);
+  // The dynamic shared-memory opt-in is per device (context): remember it per device id.
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (!bit || !(attr_set.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(attn_kernel<D, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   attn_kernel<D, M><<<num_ctas, kThreads, Cfg<D>::kSmem, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_attention(const AttnParams &p, int head_dim, int num_ctas, cudaStream_t s) {
+  if (p.mc_o)
+    return head_dim == 128 ? launch_attention_t<128, kOutMulticast>(p, num_ctas, s)
+                           : launch_attention_t<64, kOutMulticast>(p, num_ctas, s);
   if (p.n_ox > 0)
-    return head_dim == 128 ? launch_attention_t<128, true>(p, num_ctas, s)
-                           : launch_attention_t<64, true>(p, num_ctas, s);
-  return head_dim == 128 ? launch_attention_t<128, false>(p, num_ctas, s)
-                         : launch_attention_t<64, false>(p, num_ctas, s);
+    return head_dim == 128 ? launch_attention_t<128, kOutExtra>(p, num_ctas, s)
+                           : launch_attention_t<64, kOutExtra>(p, num_ctas, s);
+  return head_dim == 128 ? launch_attention_t<128, kOutSingle>(p, num_ctas, s)
+                         : launch_attention_t<64, kOutSingle>(p, num_ctas, s);
 }
 
-cudaError_t launch_merge(const AttnParams &p, int head_dim, int hkv, cudaStream_t s) {
+// Warps per merged row: enough that the split-K chunks of a row (s_max <= 8 at C3 on one
+// GPU, up to 64-128 on an 8-way head shard) spread over the whole GPU.
+template <int D>
+static cudaError_t launch_merge_t(const AttnParams &p, int64_t rows, cudaLaunchConfig_t &cfg) {
+  const int w = p.s_max <= 8 ? 1 : p.s_max <= 16 ? 2 : p.s_max <= 32 ? 4 : 8;
+  const int64_t rpb = 8 / w;
+  cfg.gridDim = dim3((unsigned)((rows + rpb - 1) / rpb));
+  switch (w) {
+    case 1: return cudaLaunchKernelEx(&cfg, merge_kernel<D, 1>, p);
+    case 2: return cudaLaunchKernelEx(&cfg, merge_kernel<D, 2>, p);
+    case 4: return cudaLaunchKernelEx(&cfg, merge_kernel<D, 4>, p);
+    default: return cudaLaunchKernelEx(&cfg, merge_kernel<D, 8>, p);
+  }
+}
+
+cudaError_t launch_merge(const AttnParams &p, int head_dim, int hkv, cudaStream_t s, bool pdl) {
   const int64_t rows = (int64_t)hkv * p.n_last_pairs * 2 * kTileRows;
-  const unsigned blocks = (unsigned)((rows + 7) / 8);
-  if (blocks == 0) return cudaSuccess;
-  if (head_dim == 128)
-    merge_kernel<128><<<blocks, 256, 0, s>>>(p);
-  else
-    merge_kernel<64><<<blocks, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  if (rows == 0) return cudaSuccess;
+  // Programmatic dependent launch (merge_output follows the split-K pass):
+  // the merge grid is launched while the attention grid drains.
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return head_dim == 128 ? launch_merge_t<128>(p, rows, cfg) : launch_merge_t<64>(p, rows, cfg);
 }
 
 }  // namespace ta

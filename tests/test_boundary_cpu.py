@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert ta.abi_version() == 3
+    assert ta.abi_version() == 4
 
 
 def test_status_strings():

@@ -81,9 +81,11 @@ def test_qwen_shape_g7(n):
     _full_parity(28, 4, n, 128, 8, 512, 128, False, seed=n + 2)
 
 
+@pytest.mark.parametrize("dense", [False, True])
 @pytest.mark.parametrize("dist", ["large", "sink"])
-def test_stress_distributions(dist):
-    _full_parity(8, 2, 2500, 128, 8, 512, 128, False, seed=77, dist=dist)
+def test_stress_distributions(dist, dense):
+    """SURVEY 8(c) stress distributions at the full Llama head count (32 q / 8 kv heads)."""
+    _full_parity(32, 8, 4097, 128, 8, 512, 128, dense, seed=77, dist=dist)
 
 
 def test_token_major_layout_and_lse():
@@ -145,10 +147,18 @@ def test_final_layer_last_rows_full_size():
 
 
 # ---------------------------------------------------------------- structural pins
-def test_v_ones_gives_ones():
-    q, k, v = synth.make_qkv(32, 8, 3000, 128, seed=11, dist="ones_v")
-    o, _ = _run(q, k, v, 8, 512, 128, False)
-    assert (o - 1.0).abs().max().item() <= 2 ** -7
+@pytest.mark.parametrize("mode", ["triangle", "dense", "last_rows", "qwen"])
+def test_v_ones_gives_ones(mode):
+    """V = 1 => O = 1.0 bit-exact: the row sum normalises exactly the bf16 P
+    that the PV MMA consumes, so every weight set sums to one in O and in l alike."""
+    hq, hkv = (28, 4) if mode == "qwen" else (32, 8)
+    q, k, v = synth.make_qkv(hq, hkv, 3000, 128, seed=11, dist="ones_v")
+    if mode == "last_rows":
+        dev = torch.device("cuda")
+        o = ta.last_rows_attn_prefill(q.to(dev), k.to(dev), v.to(dev), last_q=200).float().cpu()
+    else:
+        o, _ = _run(q, k, v, 8, 512, 128, mode == "dense")
+    assert torch.equal(o, torch.ones_like(o))
 
 
 def test_zero_q_onehot_v_exact_counts():
@@ -218,6 +228,25 @@ def test_full_size_sampled_rows(name):
     rows = _sample_rows(c.n, c.last, np.random.default_rng(0))
     o_ref, lse_ref, _ = cref.attention(q, k, v, c.si, c.sl, c.last, False, rows=rows)
     _compare(o[:, rows], o_ref, name)
+    assert np.abs(lse[:, rows].double().numpy() - lse_ref).max() < 2e-3
+
+
+def _dense_sample_rows(n, rng):
+    rows = set(range(0, 64)) | set(range(n - 32, n)) | set(range(n // 2 - 8, n // 2 + 8))
+    rows |= set(rng.choice(n, 96, replace=False).tolist())
+    return np.array(sorted(rows))
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_full_size_dense_sampled_rows(name):
+    """The dense causal layer -- the speedup denominator -- at the
+    bench's full size, on oracle-computed sampled rows (first, middle, last, random)."""
+    c = synth.CONFIGS[name]
+    q, k, v = synth.config_qkv(c, layer=0)
+    o, lse = _run(q, k, v, 0, 1, 1, True, lse=True)
+    rows = _dense_sample_rows(c.n, np.random.default_rng(1))
+    o_ref, lse_ref, _ = cref.attention(q, k, v, 0, 1, 1, True, rows=rows)
+    _compare(o[:, rows], o_ref, name + " dense")
     assert np.abs(lse[:, rows].double().numpy() - lse_ref).max() < 2e-3
 
 
