@@ -53,11 +53,13 @@ def parse():
     ap.add_argument("--l2", choices=["flush", "inputs"], default="flush",
                     help="between timed steps: write a 512 MiB buffer (flush), or rely on the "
                          "inputs (1.5 GB at C3) exceeding the 126 MB L2 (inputs)")
-    ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
+    ap.add_argument("--gather", choices=["nccl", "fused", "multicast"], default="nccl",
                     help="N>1: O all-gather by NCCL after the kernel, or fused into the kernel "
                          "epilogue (f2: *_multi entry points storing into peer ranks' symmetric-"
                          "memory O buffers over NVLink; checked against NCCL once, falls back "
-                         "to NCCL if the symmetric-memory rendezvous or the check fails)")
+                         "to NCCL if the symmetric-memory rendezvous or the check fails), or fused "
+                         "with multimem stores to the symmetric buffer's NVLS multicast address "
+                         "(one egress per tile; same check and fallback)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-points", action="store_true",
                     help="skip the C2 / Qwen 64K / Qwen 128K points and the shard-shape points")
@@ -350,7 +352,7 @@ def main():
     layer = layer_nccl
     gather_mode = "nccl" if world > 1 else None
     o_result = od   # the buffer holding this rank's O after a step (e2e reads it back)
-    if world > 1 and args.gather == "fused":
+    if world > 1 and args.gather in ("fused", "multicast"):
         # f2: every rank's epilogue stores its O tiles into all ranks' symmetric-memory
         # full-O buffers (own slice + the same head slice of each peer); a device-side
         # barrier orders them before the next layer reads.  Verified once against NCCL.
@@ -362,9 +364,20 @@ def main():
             peers = [hdl.get_buffer(r, (c.hq, c.n, c.d), torch.bfloat16)[h0:h1]
                      for r in range(world) if r != rank]
             own = o_sym[h0:h1]
+            mc_ptr = int(getattr(hdl, "multicast_ptr", 0) or 0) if args.gather == "multicast" else 0
+            if args.gather == "multicast" and not mc_ptr:
+                raise RuntimeError("symmetric memory has no multicast (NVLS) address on this box")
+            mc_slice = mc_ptr + h0 * c.n * c.d * 2   # this rank's heads inside the full O
 
             def layer_fused(dense=False):
-                if dense:
+                if mc_ptr:   # one multimem store per tile; the NVSwitch replicates it
+                    if dense:
+                        ta.dense_attn_prefill_multicast(qd, kd, vd, mc_slice, (c.n * c.d, c.d), own)
+                    else:
+                        ta.triangle_attn_prefill_multicast(qd, kd, vd, mc_slice, (c.n * c.d, c.d),
+                                                           own, sink=c.si, window=c.sl,
+                                                           last_q=c.last)
+                elif dense:
                     ta.dense_attn_prefill_multi(qd, kd, vd, peers, own)
                 else:
                     ta.triangle_attn_prefill_multi(qd, kd, vd, peers, own, sink=c.si, window=c.sl,
@@ -377,7 +390,9 @@ def main():
             ok = torch.tensor([1.0 if torch.equal(o_sym, o_full) else 0.0], device=dev)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if ok.item() == 1.0:
-                layer, gather_mode = layer_fused, "fused (kernel epilogue -> peer symmetric memory)"
+                layer, gather_mode = layer_fused, ("fused multicast (kernel epilogue multimem stores "
+                                                   "-> NVLS)" if mc_ptr else
+                                                   "fused (kernel epilogue -> peer symmetric memory)")
                 o_result = own
             else:
                 gather_mode = "nccl (fused output check failed)"

@@ -13,30 +13,32 @@ Spec summary:
     LASTQ items of the last pairs (no STREAM items); header kind field 2.
     STREAM(kvh, p), p < p_last0: band [max(si, r0-sl+1), r1+1) (empty -> [r1+1, r1+1));
        sink [0, min(si, r1+1)) implicit.
-    LASTQ(kvh, p, c): [c*ck, min((c+1)*ck, r1+1)) for c < ceil((r1+1)/ck).
   dense: DENSE(kvh, p) = [0, r1+1).
   blocks: each key range cut at 128, width rounded up to 16; STREAM sink range first.
   cost = sum of block widths + 192 (per-item overhead: epilogue, pipeline turn-around).
-  ck = largest power of two <= C_tot // (8 num_ctas) clamped to [512, 16384]
-       (4 num_ctas in the last-rows mode)
-       (C_tot: all STREAM items + one unsplit LASTQ item per last pair, all kv heads).
-  canonical order: LASTQ (kvh, p, c) then STREAM/DENSE (kvh, p);
-  LPT: stable sort by cost descending; each to least-loaded CTA, ties lowest id.
-  bytes: 16 x u32 header, u32 offsets[num_ctas+1], 16-byte items
-         {u8 kind, u8 0, u16 kvh, u32 pair, u32 key_begin, u32 key_end}.
+  1. LPT of the STREAM / DENSE items (canonical order (kvh, p)): stable sort by cost
+     descending; each to the least-loaded CTA, ties to the lowest CTA id.
+  2. Water-filling of the Last Q-K work (schedule version 2): the spans [0, r1+1) of the
+     last pairs, canonical order (kvh, p), are cut into 128-key blocks; B = total blocks.
+     Level L = the smallest integer with sum_c max(0, (L - load_c - 192) // 128) >= B.
+     CTAs in order (load, id) ascending each take the next min(rem, cap_c) blocks of the
+     span sequence; a take is cut at span ends into LASTQ(kvh, p) pieces
+     [b0*128, min(b1*128, r1+1)) appended to that CTA's list; a piece's chunk index (u8
+     item field `pad`) is its ordinal within its span.  s_max = max pieces per span.
+  bytes: 16 x u32 header (version 2; field 12 = 0: variable pieces), u32
+         offsets[num_ctas+1], 16-byte items {u8 kind, u8 chunk, u16 kvh, u32 pair,
+         u32 key_begin, u32 key_end}.
 """
 from __future__ import annotations
 
 import struct
 
 STREAM, LASTQ, DENSE = 0, 1, 2
-MAGIC, VERSION = 0x43534154, 1
+MAGIC, VERSION = 0x43534154, 2
 
 
 
 ITEM_OVERHEAD = 192  # LPT cost of an item beyond its key columns (DESIGN.md section 4)
-CK_DIV = 8           # chunk_keys target: C_tot / (CK_DIV * num_ctas)
-CK_DIV_LAST_ROWS = 4  # ... in the final-layer last-rows mode (LASTQ items only)
 
 def _r16(x):
     return -(-x // 16) * 16
@@ -80,7 +82,7 @@ def item_blocks(geo, it):
     width = 16 + round16(min(112, band length)); used for STREAM items whose sink span
     min(si, r1+1) is in 1..16.
     """
-    kind, kvh, p, kb, ke = it
+    kind, kvh, p, kb, ke = it[:5]
     bl = []
     if kind == STREAM:
         r0, r1 = rows(geo, p)
@@ -105,47 +107,47 @@ def stream_item(geo, kvh, p):
     return (STREAM, kvh, p, min(b0, b1), b1)
 
 
-def chunk_keys(geo, num_ctas):
-    if geo["dense"]:
-        return 0
-    tot = 0
-    for p in range(0 if geo["last_rows"] else geo["p_last0"]):
-        tot += cost(geo, stream_item(geo, 0, p))
-    for p in range(geo["p_last0"], geo["pairs"]):
-        tot += cost(geo, (LASTQ, 0, p, 0, rows(geo, p)[1] + 1))
-    tot *= geo["hkv"]
-    target = tot // ((CK_DIV_LAST_ROWS if geo["last_rows"] else CK_DIV) * num_ctas)
-    ck = 512
-    while ck * 2 <= target and ck * 2 <= 16384:
-        ck *= 2
-    return ck
-
-
-def enumerate_items(geo, ck):
+def base_items(geo):
+    """STREAM (triangle) or DENSE items in canonical order (kvh, p); 6-tuples with pad 0."""
     items = []
     if geo["dense"]:
         for kvh in range(geo["hkv"]):
             for p in range(geo["pairs"]):
-                items.append((DENSE, kvh, p, 0, rows(geo, p)[1] + 1))
-        return items
-    for kvh in range(geo["hkv"]):
-        for p in range(geo["p_last0"], geo["pairs"]):
-            span = rows(geo, p)[1] + 1
-            for c in range(-(-span // ck)):
-                items.append((LASTQ, kvh, p, c * ck, min((c + 1) * ck, span)))
-    if not geo["last_rows"]:
+                items.append((DENSE, kvh, p, 0, rows(geo, p)[1] + 1, 0))
+    elif not geo["last_rows"]:
         for kvh in range(geo["hkv"]):
             for p in range(geo["p_last0"]):
-                items.append(stream_item(geo, kvh, p))
+                items.append(stream_item(geo, kvh, p) + (0,))
     return items
 
 
+def last_spans(geo):
+    """(kvh, pair, keys) of every last pair, canonical order; keys = r1 + 1."""
+    if geo["dense"]:
+        return []
+    return [(kvh, p, rows(geo, p)[1] + 1) for kvh in range(geo["hkv"])
+            for p in range(geo["p_last0"], geo["pairs"])]
+
+
+def fill_level(load, nblocks):
+    """Smallest integer L with sum_c max(0, (L - load_c - ITEM_OVERHEAD) // 128) >= nblocks."""
+    def cap(L):
+        return sum(max(0, (L - x - ITEM_OVERHEAD) // 128) for x in load)
+    lo, hi = 0, max(load) + ITEM_OVERHEAD + 128 * nblocks
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if cap(mid) >= nblocks:
+            hi = mid
+        else:
+            lo = mid + 1
+    return lo
+
+
 def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False):
-    """Returns (geo, ck, s_max, per_cta_lists)."""
+    """Returns (geo, 0, s_max, per_cta_lists, loads); items are 6-tuples
+    (kind, kvh, pair, key_begin, key_end, chunk)."""
     geo = geometry(n, hq, hkv, d, si, sl, last, dense, last_rows)
-    ck = chunk_keys(geo, num_ctas)
-    s_max = 0 if dense else -(-n // ck)
-    items = enumerate_items(geo, ck)
+    items = base_items(geo)
     costs = [cost(geo, it) for it in items]
     order = sorted(range(len(items)), key=lambda i: (-costs[i], i))
     load = [0] * num_ctas
@@ -154,7 +156,33 @@ def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False):
         c = min(range(num_ctas), key=lambda x: (load[x], x))
         per[c].append(items[i])
         load[c] += costs[i]
-    return geo, ck, s_max, per, load
+    spans = last_spans(geo)
+    nblk = [-(-keys // 128) for (_, _, keys) in spans]
+    total = sum(nblk)
+    s_max = 0
+    if total:
+        L = fill_level(load, total)
+        caps = [max(0, (L - x - ITEM_OVERHEAD) // 128) for x in load]
+        si_, off, rem = 0, 0, total
+        pieces = [0] * len(spans)
+        for c in sorted(range(num_ctas), key=lambda x: (load[x], x)):
+            take = min(rem, caps[c])
+            while take > 0:
+                kvh, p, keys = spans[si_]
+                k = min(take, nblk[si_] - off)
+                it = (LASTQ, kvh, p, off * 128, min((off + k) * 128, keys), pieces[si_])
+                per[c].append(it)
+                load[c] += cost(geo, it)
+                pieces[si_] += 1
+                off += k
+                take -= k
+                rem -= k
+                if off == nblk[si_]:
+                    si_, off = si_ + 1, 0
+            if rem == 0:
+                break
+        s_max = max(pieces)
+    return geo, 0, s_max, per, load
 
 
 def serialize(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False) -> bytes:
@@ -162,15 +190,15 @@ def serialize(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False) -> 
     nitems = sum(len(x) for x in per)
     kind = 1 if dense else (2 if geo["last_rows"] else 0)
     hdr = [MAGIC, VERSION, kind, n, hq, hkv, d, geo["si"], geo["sl"], geo["last"],
-           geo["T"], 2, ck, num_ctas, nitems, s_max]
+           geo["T"], 2, 0, num_ctas, nitems, s_max]
     out = struct.pack("<16I", *hdr)
     off = [0]
     for x in per:
         off.append(off[-1] + len(x))
     out += struct.pack("<%dI" % len(off), *off)
     for x in per:
-        for kind, kvh, p, kb, ke in x:
-            out += struct.pack("<BBHIII", kind, 0, kvh, p, kb, ke)
+        for kind, kvh, p, kb, ke, ch in x:
+            out += struct.pack("<BBHIII", kind, ch, kvh, p, kb, ke)
     return out
 
 
@@ -181,4 +209,4 @@ def parse(buf: bytes):
     off = list(struct.unpack_from("<%dI" % (num_ctas + 1), buf, 64))
     base = 64 + 4 * (num_ctas + 1)
     items = [struct.unpack_from("<BBHIII", buf, base + 16 * i) for i in range(nitems)]
-    return hdr, off, [(k, kvh, p, kb, ke) for (k, _, kvh, p, kb, ke) in items]
+    return hdr, off, [(k, kvh, p, kb, ke, ch) for (k, ch, kvh, p, kb, ke) in items]

@@ -95,12 +95,41 @@ struct DevSchedule {
   ta::Geometry g;
   ta::Item *d_items = nullptr;
   uint32_t *d_offsets = nullptr;
+  uint8_t *d_span = nullptr;  // LASTQ pieces per (kvh, last pair), read by the merge
   int num_ctas = 0;
 };
 
 typedef std::tuple<int, int64_t, int, int, int, int, int, int, int, int, int> SchedKey;
 std::mutex g_mu;
 std::map<SchedKey, DevSchedule> g_sched;
+std::map<SchedKey, int> g_host_smax;  // s_max of host-built schedules (workspace queries)
+
+SchedKey sched_key(int dev, const ta::Geometry &g, int num_ctas) {
+  return SchedKey(dev, g.n, g.hq, g.hkv, g.d, g.dense ? 1 : 0, g.last_only ? 1 : 0, g.si, g.sl,
+                  g.last, num_ctas);
+}
+
+// Persistent CTAs per launch: one per SM (chunk indices are u8: at most kMaxCtas).
+int ctas_for(int sms) { return std::max(1, std::min(sms, ta::kMaxCtas)); }
+
+// Geometry with s_max filled in (the water-filled schedule decides it), host only, cached.
+ta::Geometry planned_geometry(const ta::Geometry &g0, int num_ctas) {
+  ta::Geometry g = g0;
+  if (g.dense) return g;
+  const SchedKey key = sched_key(-1, g0, num_ctas);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_host_smax.find(key);
+    if (it != g_host_smax.end()) {
+      g.s_max = it->second;
+      return g;
+    }
+  }
+  g = ta::build_schedule(g0, num_ctas).g;
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_host_smax[key] = g.s_max;
+  return g;
+}
 
 struct DeviceInfo {
   int sms = 0, major = 0, minor = 0;
@@ -132,8 +161,7 @@ ta_status device_info(int *dev, DeviceInfo *info) {
 }
 
 ta_status get_schedule(int dev, const ta::Geometry &g, int num_ctas, DevSchedule *out) {
-  SchedKey key(dev, g.n, g.hq, g.hkv, g.d, g.dense ? 1 : 0, g.last_only ? 1 : 0, g.si, g.sl, g.last,
-               num_ctas);
+  const SchedKey key = sched_key(dev, g, num_ctas);
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_sched.find(key);
   if (it != g_sched.end()) {
@@ -146,14 +174,19 @@ ta_status get_schedule(int dev, const ta::Geometry &g, int num_ctas, DevSchedule
   ds.num_ctas = num_ctas;
   const size_t ib = std::max<size_t>(1, s.items.size()) * sizeof(ta::Item);
   const size_t ob = s.offsets.size() * sizeof(uint32_t);
+  const size_t sb = std::max<size_t>(1, s.span_pieces.size());
   cudaError_t e = cudaMalloc(&ds.d_items, ib);
   if (e == cudaSuccess) e = cudaMalloc(&ds.d_offsets, ob);
+  if (e == cudaSuccess) e = cudaMalloc(&ds.d_span, sb);
+  if (e == cudaSuccess && !s.span_pieces.empty())
+    e = cudaMemcpy(ds.d_span, s.span_pieces.data(), s.span_pieces.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !s.items.empty())
     e = cudaMemcpy(ds.d_items, s.items.data(), s.items.size() * sizeof(ta::Item), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(ds.d_offsets, s.offsets.data(), ob, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(ds.d_items);
     cudaFree(ds.d_offsets);
+    cudaFree(ds.d_span);
     return fail(TA_ERR_CUDA, std::string("schedule upload: ") + cudaGetErrorString(e));
   }
   g_sched.emplace(key, ds);
@@ -256,15 +289,16 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
   ta::Geometry g;
   std::string err;
   if (!call_geometry(p, tri, mode, last_q, &g, &err)) return fail(TA_ERR_SHAPE, err);
-  ta::plan_chunks(&g, di.sms);
-  const size_t need = ta::workspace_bytes(g);
+  // The schedule (host build + one upload per device and signature, cached) fixes s_max
+  // and so the workspace size; nothing is enqueued before the checks below.
+  DevSchedule ds;
+  if ((s = get_schedule(dev, g, ctas_for(di.sms), &ds)) != TA_OK) return s;
+  const size_t need = ta::workspace_bytes(ds.g);
   if (need > 0) {
     if (!ws) return fail(TA_ERR_WORKSPACE, "workspace is NULL");
     if (ws_bytes < need) return fail(TA_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
     if (reinterpret_cast<uintptr_t>(ws) & 255u) return fail(TA_ERR_WORKSPACE, "workspace not 256-byte aligned");
   }
-  DevSchedule ds;
-  if ((s = get_schedule(dev, g, di.sms, &ds)) != TA_OK) return s;
 
   ta::AttnParams prm;
   std::memset(&prm, 0, sizeof(prm));
@@ -332,6 +366,7 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
   prm.n_last_pairs = (int)ds.g.n_last_pairs;
   prm.chunk_keys = ds.g.chunk_keys;
   prm.s_max = ds.g.s_max;
+  prm.span_pieces = ds.d_span;
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / std::sqrt((float)g.d);
   prm.scale = scale;
   prm.scale_log2 = scale * 1.4426950408889634f;
@@ -408,8 +443,7 @@ size_t ws_size(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t l
   } else {
     cudaGetLastError();
   }
-  ta::plan_chunks(&g, sms);
-  return ta::workspace_bytes(g);
+  return ta::workspace_bytes(planned_geometry(g, ctas_for(sms)));
 }
 
 }  // namespace
@@ -535,7 +569,8 @@ ta_status export_schedule(const ta_problem *p, const ta_triangle *tri, Mode mode
     if (s != TA_OK) return s;
     if (mode == kTriangle && (s = validate_triangle(tri)) != TA_OK) return s;
     if (mode == kLastRows && last_q < 1) return fail(TA_ERR_PARAMS, "last_q < 1 (final-layer rows)");
-    if (num_ctas < 1) return fail(TA_ERR_PARAMS, "num_ctas < 1");
+    if (num_ctas < 1 || num_ctas > ta::kMaxCtas)
+      return fail(TA_ERR_PARAMS, "num_ctas must be in [1, " + std::to_string(ta::kMaxCtas) + "]");
     ta::Geometry g;
     std::string err;
     if (!call_geometry(p, tri, mode, last_q, &g, &err)) return fail(TA_ERR_SHAPE, err);
@@ -658,8 +693,10 @@ void ta_release_caches(void) {
   for (auto &kv : g_sched) {
     cudaFree(kv.second.d_items);
     cudaFree(kv.second.d_offsets);
+    cudaFree(kv.second.d_span);
   }
   g_sched.clear();
+  g_host_smax.clear();
 }
 
 }  // extern "C"

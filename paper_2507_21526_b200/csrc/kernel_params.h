@@ -29,6 +29,7 @@ struct alignas(64) AttnParams {
   float *part_lse;   // [slot][2*128 rows] fp32 natural-log LSE_c
   const Item *items;
   const uint32_t *offsets;
+  const uint8_t *span_pieces;  // LASTQ pieces per (kvh, last pair) = merge chunk counts
   int n, hq, group, tile_tokens, pair_tokens;
   int si, sl, last, dense;
   int last_only;     // final-layer mode: the merge writes only rows >= N - last ...

@@ -176,6 +176,29 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_EARLY_K
 #define TA_EARLY_K 0
 #endif
+// Timing-only experiments (wrong results; never in a shipped build): skip the epilogue's
+// work (NOEPI) or load Q only for a CTA's first item (QONCE).
+#ifndef TA_EXP_NOEPI
+#define TA_EXP_NOEPI 0
+#endif
+#ifndef TA_EXP_QONCE
+#define TA_EXP_QONCE 0
+#endif
+#ifndef TA_EXP_NOMASK  // timing only: no kept-column masking (wrong results)
+#define TA_EXP_NOMASK 0
+#endif
+#ifndef TA_SKIP_RAGGED  // exponentials only over the block's computed 16-column chunks
+#define TA_SKIP_RAGGED 0
+#endif
+#ifndef TA_MASK_VOTE
+#define TA_MASK_VOTE 0
+#endif
+#ifndef TA_EPI_FMUL2
+#define TA_EPI_FMUL2 0
+#endif
+#ifndef TA_ITEM_PREFETCH  // every role loads its next schedule item one item ahead
+#define TA_ITEM_PREFETCH 0   // measured +5 % cycles (C3, dense): the extra live registers
+#endif                       // cost the softmax more than the hidden load latency saves
 #ifndef TA_PINGPONG
 #define TA_PINGPONG 0
 #endif
@@ -191,6 +214,34 @@ constexpr bool kPingPong = TA_PINGPONG != 0;
 #ifndef TA_DELAY_TMA
 #define TA_DELAY_TMA 0
 #endif
+// Wait accounting (TA_WAITSTAT builds, with TA_CTA_CLOCK): each role sums the SM cycles it
+// spends in each barrier wait; written at the end to trace[4096 + 64 cta + 8 role + k]
+// (roles: 0 TMA producer, 1 MMA issuer, 2/3 softmax tile A/B (warp quarter 0, lane 0),
+// 4 epilogue (warp 0, lane 0)); scripts/waitstat.py prints them.
+#ifdef TA_WAITSTAT
+#define WS_DECL long long ws_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define WS(k, ...)                          \
+  do {                                      \
+    const long long ws_t0_ = clock64();     \
+    __VA_ARGS__;                            \
+    ws_acc[k] += clock64() - ws_t0_;        \
+  } while (0)
+#define WS_DUMP(role, cond)                                                          \
+  do {                                                                              \
+    if (cond)                                                                       \
+      for (int k_ = 0; k_ < 8; ++k_) p.trace[4096 + 64 * blockIdx.x + 8 * (role) + k_] = ws_acc[k_]; \
+  } while (0)
+#else
+#define WS_DECL
+#define WS(k, ...) \
+  do {             \
+    __VA_ARGS__;   \
+  } while (0)
+#define WS_DUMP(role, cond) \
+  do {                      \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void spin_cycles(int n) {
   if (n > 0) {
     const long long t0 = clock64();
@@ -204,6 +255,7 @@ struct ItemInfo {
   int kb0, ke0;   // item key range (band / chunk / causal)
   int r0, r1;     // token rows of the pair, clipped to N
   int fused;      // STREAM: sink (<= 16 keys) folded into block 0
+  int chunk;      // LASTQ: piece index within the pair's span (split-K slot)
   int s_end, ns;  // STREAM unfused: sink keys [0, s_end) in ns blocks of their own
   int nb;         // total key blocks
 };
@@ -225,6 +277,7 @@ __device__ __forceinline__ void item_info(const AttnParams &p, const Item &it, I
   f.pair = (int)it.pair;
   f.kb0 = (int)it.key_begin;
   f.ke0 = (int)it.key_end;
+  f.chunk = it.pad;
   f.r0 = f.pair * p.pair_tokens;
   f.r1 = min(f.r0 + p.pair_tokens, p.n) - 1;
   f.fused = 0;
@@ -243,6 +296,35 @@ __device__ __forceinline__ void item_info(const AttnParams &p, const Item &it, I
   }
   f.nb = f.ns + ceil_div(len, kBlockKeys);
 }
+
+// One 16-byte schedule item (read-only path).
+__device__ __forceinline__ Item item_at(const AttnParams &p, uint32_t i) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p.items) + i);
+  Item it;
+  it.kind = (uint8_t)(v.x & 0xff);
+  it.pad = (uint8_t)((v.x >> 8) & 0xff);  // LASTQ chunk index
+  it.kv_head = (uint16_t)(v.x >> 16);
+  it.pair = v.y;
+  it.key_begin = v.z;
+  it.key_end = v.w;
+  return it;
+}
+
+// Per-role item stream: item ii is in registers when the role reaches it (its global load
+// was issued one item earlier, off the hand-off paths).
+struct ItemStream {
+  Item nxt;
+  uint32_t end;
+  __device__ __forceinline__ ItemStream(const AttnParams &p, uint32_t beg, uint32_t e) : end(e) {
+    if (TA_ITEM_PREFETCH && beg < e) nxt = item_at(p, beg);
+  }
+  __device__ __forceinline__ Item take(const AttnParams &p, uint32_t ii) {
+    if (!TA_ITEM_PREFETCH) return item_at(p, ii);
+    const Item cur = nxt;
+    if (ii + 1 < end) nxt = item_at(p, ii + 1);
+    return cur;
+  }
+};
 
 __device__ __forceinline__ Blk block_info(const ItemInfo &f, int j) {
   Blk b;
@@ -510,6 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   if (warp == kTmaWarp) {
     // ===================== TMA producer (whole warp, one elected lane issues) ==========
     const bool leader = ptx::elect_one();
+    WS_DECL;
     {
 #ifdef TA_TRACE
       uint32_t trc = 0;
@@ -522,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       uint32_t seq = 0, nitem = 0;
       const uint32_t q_bytes = 2u * C::kHalves * 128u * p.tile_tokens * p.group;
       auto load_q = [&](const ItemInfo &f, uint32_t nitem) {
-        ptx::mbar_wait_lazy(q_empty, (nitem & 1u) ^ 1u);
+        WS(0, ptx::mbar_wait_lazy(q_empty, (nitem & 1u) ^ 1u));
         if (leader) {
           ptx::mbar_arrive_expect_tx(q_full, q_bytes);
           for (int x = 0; x < 2; ++x)
@@ -538,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         for (int kv = 0; kv < 2; ++kv, ++seq) {
           uint32_t slot, ph;
           ring_pos(seq, C::kStages, slot, ph);
-          ptx::mbar_wait_lazy(&kv_empty[slot], ph ^ 1u);
+          WS(1, ptx::mbar_wait_lazy(&kv_empty[slot], ph ^ 1u));
           if (leader) {
             uint64_t *const fb = &kv_full[slot];
             // one 128-row box, or 16 sink rows + a 112-row band box (fused first block)
@@ -563,25 +646,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       // Q(i) (which waits for the previous item's last QK^T) follows; the next item's Q
       // tiles are prefetched into L2 one item ahead so the Q load at the item boundary is
       // an L2 hit rather than an HBM round trip.
+      ItemStream is(p, it_beg, it_end);
       for (uint32_t ii = it_beg; ii < it_end; ++ii, ++nitem) {
         ItemInfo f;
-        item_info(p, p.items[ii], f);
+        item_info(p, is.take(p, ii), f);
         if (leader && ii + 1 < it_end) {
           ItemInfo fn;
-          item_info(p, p.items[ii + 1], fn);
+          item_info(p, TA_ITEM_PREFETCH ? is.nxt : item_at(p, ii + 1), fn);
           for (int x = 0; x < 2; ++x)
             for (int h = 0; h < C::kHalves; ++h)
               ptx::tma_prefetch_l2_3d(&p.tm_q, h * 64, fn.r0 + x * p.tile_tokens, fn.kvh * p.group);
         }
         load_kv(f, 0);
-        load_q(f, nitem);
+        if (!TA_EXP_QONCE || nitem == 0) load_q(f, nitem);
         for (int j = 1; j < f.nb; ++j) load_kv(f, j);
       }
     }
+    WS_DUMP(0, leader);
     __syncwarp();
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (whole warp, one elected lane issues) ============
     const bool leader = ptx::elect_one();
+    WS_DECL;
     {
 #ifdef TA_TRACE
       uint32_t trc = 0;
@@ -643,11 +729,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       // block j+1 may be block 0 of the next item, so a new item's first QK^T overlaps the
       // previous item's last softmax instead of draining the pipeline.
       if (it_beg < it_end) {
+        ItemStream is(p, it_beg, it_end);
         ItemInfo f;
-        item_info(p, p.items[it_beg], f);
+        item_info(p, is.take(p, it_beg), f);
         uint32_t ii = it_beg;
         int j = 0;
-        MMA_WAIT(q_full, nitem & 1u);
+        WS(0, MMA_WAIT(q_full, nitem & 1u));
         ptx::tc_fence_after();
         TRACE_MM(16, nitem);
         Blk b = block_info(f, 0);
@@ -665,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           opaque_bases();
           ring_pos(seq + 1, C::kStages, vslot, vph);
           TRACE_MM(9, j);
-          MMA_WAIT(&kv_full[vslot], vph);
+          WS(1, MMA_WAIT(&kv_full[vslot], vph));
           for (int w = 0; w < TA_EXTRA_WAITS; ++w) MMA_WAIT(&kv_full[vslot], vph);
           TRACE_MM(17, j);
           // next block in the flat stream (same item j+1, or block 0 of the next item)
@@ -674,7 +761,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           ItemInfo f1 = f;
           int j1 = j + 1;
           if (last && more) {
-            item_info(p, p.items[ii + 1], f1);
+            item_info(p, is.take(p, ii + 1), f1);
             j1 = 0;
           }
           Blk b1 = b;
@@ -690,16 +777,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(8, j);
           spin_cycles(TA_DELAY_MMA);
           if (TA_PV_SPLIT) {
-            MMA_WAIT(&p_ready[0], pph[0]);
+            WS(3, MMA_WAIT(&p_ready[0], pph[0]));
             pph[0] ^= 1u;
             ptx::tc_fence_after();
           }
           TRACE_MM(10, j);
           const uint32_t kitem = ii - it_beg;  // item of block j
-          if (j == 0 && kitem > 0) MMA_WAIT(&o_free[0], (kitem - 1) & 1u);  // O_A drained
+          if (j == 0 && kitem > 0) WS(5, MMA_WAIT(&o_free[0], (kitem - 1) & 1u));  // O_A drained
           if (TA_PV_SPLIT) {
             issue_pv(0, vslot, f, b, j > 0, 0);  // keys 0..63 while the softmax finishes 64..127
-            MMA_WAIT(&p_hi[0], pph[0] ^ 1u);
+            WS(4, MMA_WAIT(&p_hi[0], pph[0] ^ 1u));
           } else {
             MMA_WAIT(&p_hi[0], pph[0]);
             pph[0] ^= 1u;
@@ -712,11 +799,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           if (more) {
             if (last) {  // the next item's Q tiles
               ++nitem;
-              MMA_WAIT(q_full, nitem & 1u);
+              if (!TA_EXP_QONCE) WS(0, MMA_WAIT(q_full, nitem & 1u));
               TRACE_MM(16, nitem);
             }
             TRACE_MM(18, j);
-            if (!TA_EARLY_K) MMA_WAIT(&kv_full[kslot1], kph1);
+            if (!TA_EARLY_K) WS(2, MMA_WAIT(&kv_full[kslot1], kph1));
             ptx::tc_fence_after();
             TRACE_MM(19, j);
             issue_qk(0, kslot1, f1, b1);
@@ -726,15 +813,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           // ---- tile B: PV_B(j), then QK_B(next)
           TRACE_MM(7, j);
           if (TA_PV_SPLIT) {
-            MMA_WAIT(&p_ready[1], pph[1]);
+            WS(6, MMA_WAIT(&p_ready[1], pph[1]));
             pph[1] ^= 1u;
             ptx::tc_fence_after();
           }
           TRACE_MM(13, j);
-          if (j == 0 && kitem > 0) MMA_WAIT(&o_free[1], (kitem - 1) & 1u);  // O_B drained
+          if (j == 0 && kitem > 0) WS(5, MMA_WAIT(&o_free[1], (kitem - 1) & 1u));  // O_B drained
           if (TA_PV_SPLIT) {
             issue_pv(1, vslot, f, b, j > 0, 0);  // keys 0..63 while the softmax finishes 64..127
-            MMA_WAIT(&p_hi[1], pph[1] ^ 1u);
+            WS(7, MMA_WAIT(&p_hi[1], pph[1] ^ 1u));
           } else {
             MMA_WAIT(&p_hi[1], pph[1]);
             pph[1] ^= 1u;
@@ -759,10 +846,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
       }
     }
+    WS_DUMP(1, leader);
     __syncwarp();
   } else if (warp >= kSmWarp0 && warp < kSmWarp0 + kSoftmaxWarps) {
     // ===================== softmax / epilogue =====================
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax) : "memory");
+    WS_DECL;
     const int x = (warp - kSmWarp0) / (4 * kHPR);    // Q tile
     const int hc = ((warp - kSmWarp0) / 4) % kHPR;   // column part: S columns [kNCol hc, kNCol (hc + 1))
     const int wq = warp % 4;            // TMEM lane quarter
@@ -802,9 +891,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #ifdef TA_TRACE
     uint32_t trc = 0;
 #endif
+    ItemStream is(p, it_beg, it_end);
     for (uint32_t ii = it_beg; ii < it_end; ++ii) {
       ItemInfo f;
-      item_info(p, p.items[ii], f);
+      item_info(p, is.take(p, ii), f);
       const int tok = f.r0 + x * T + toff;     // query row i of this thread
       const bool last_row = tok >= p.n - p.last;
       float m_run = -INFINITY;  // reference max, log2 units of scaled scores
@@ -874,7 +964,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         while (!ptx::mbar_try_wait_hint(&s_full[x], sph, 1000000u)) {
         }
 #else
-        ptx::mbar_wait(&s_full[x], sph);
+        WS(0, ptx::mbar_wait(&s_full[x], sph));
 #endif
         sph ^= 1u;
         ptx::tc_fence_after();
@@ -883,7 +973,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         uint32_t s[kNCol];
         // 16-column groups this tile computes (tile_ncols; kHPR == 1): the rest of the S
         // columns hold no scores of this block and are skipped (they are masked anyway).
-        const int nch = (kHPR == 1 && TA_TILE_TRIM == 1) ? tile_ncols(f, b, x, T) / 16 : kNCol / 16;
+        const int nch = (kHPR == 1 && TA_TILE_TRIM == 1) ? tile_ncols(f, b, x, T) / 16
+                        : (kHPR == 1 && TA_SKIP_RAGGED) ? b.ncols / 16 : kNCol / 16;
         // Two halves: the second TMEM load is in flight while the first half is masked.
         if (TA_TMEM_WIDE && kHPR == 1 && TA_TILE_TRIM == 0) {  // 32-column loads
 #pragma unroll
@@ -904,13 +995,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #pragma unroll
         for (int c = 0; c < kNCol / 32; ++c) {
           if (c == kNCol / 64) ptx::tmem_wait_ld();
-          if (!warp_full && 2 * c < nch) {
+          if (!TA_EXP_NOMASK && !warp_full && 2 * c < nch) {
             // kept-column bitmask of chunk c: [a_lo, a_hi] U [b_lo, b_hi] intersected with
             // [32c, 32c + 31]
             const uint32_t m32 = iv_bits(a_lo - 32 * c, a_hi - 32 * c) | iv_bits(b_lo - 32 * c, b_hi - 32 * c);
+            // TA_MASK_VOTE: skip the selects of a 32-column chunk every row of the warp keeps
+            if (!TA_MASK_VOTE || __any_sync(0xffffffffu, m32 != 0xffffffffu)) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
-              s[c * 32 + e] = (m32 & (1u << e)) ? s[c * 32 + e] : 0xff800000u;  // -inf
+              for (int e = 0; e < 32; ++e)
+                s[c * 32 + e] = (m32 & (1u << e)) ? s[c * 32 + e] : 0xff800000u;  // -inf
+            }
           }
         }
         // raw row max over this half (scale > 0 commutes with max), then over the row
@@ -1070,7 +1164,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       {
         // Back-pressure: publish item k only after the epilogue released item k-1, so
         // l_ready never runs two phases ahead of its waiter (single-block items).
-        if (kitem_sm > 0) ptx::mbar_wait(&o_free[x], (kitem_sm - 1) & 1u);
+        if (kitem_sm > 0) WS(1, ptx::mbar_wait(&o_free[x], (kitem_sm - 1) & 1u));
         const uint32_t par = kitem_sm & 1u;
         sts_f32(ptx::smem_u32(red_l + ((par * 2 + x) * 2 + hc) * kTileRows + r), l_run);
         if (kHPR == 1) sts_f32(ptx::smem_u32(red_l + ((par * 2 + x) * 2 + 1) * kTileRows + r), 0.f);
@@ -1087,8 +1181,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #endif
       }
     }
+    WS_DUMP(2 + x, lane == 0 && wq == 0 && hc == 0);
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     // ===================== epilogue warpgroup =====================
+    WS_DECL;
     // O_x = O_x / l per row from TMEM -> bf16 global (STREAM / DENSE) or fp32 split-K
     // partial + LSE (LASTQ); then O_x's TMEM columns are released to the MMA issuer.
     const int eq = warp % 4;           // TMEM lane quarter
@@ -1103,17 +1199,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #ifdef TA_TRACE
     uint32_t trc = 0;
 #endif
+    ItemStream is(p, it_beg, it_end);
     for (uint32_t ii = it_beg; ii < it_end; ++ii, ++kitem) {
       ItemInfo f;
-      item_info(p, p.items[ii], f);
+      item_info(p, is.take(p, ii), f);
       const uint32_t par = kitem & 1u;
       for (int x = x0; x < (kEpiWarps == 8 ? x0 + 1 : 2); ++x) {
         const uint32_t tO = tmem + 256 + x * 128 + lane_off;
         const int tok = f.r0 + x * T + toff;
         const bool valid = row_in_tile && tok < p.n;
         TRACE_EP(30 + x, kitem);
-        ptx::mbar_wait_lazy(&l_ready[x], par);
-        ptx::mbar_wait_lazy(&o_full[x], par);
+        WS(0, ptx::mbar_wait_lazy(&l_ready[x], par));
+        WS(1, ptx::mbar_wait_lazy(&o_full[x], par));
         ptx::tc_fence_after();
         TRACE_EP(32 + x, kitem);
         const float l_row = lds_f32(ptx::smem_u32(red_l + ((par * 2 + x) * 2 + 0) * kTileRows + r)) +
@@ -1121,9 +1218,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const float m_row = lds_f32(ptx::smem_u32(red_m + (par * 2 + x) * kTileRows + r));
         const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
         const float lse = l_row > 0.f ? (m_row + __log2f(l_row)) * kLn2 : -INFINITY;
-        if (f.kind == kLastQ) {
+        if (TA_EXP_NOEPI) {
+        } else if (f.kind == kLastQ) {
           const int64_t slot =
-              ((int64_t)f.kvh * p.n_last_pairs + (f.pair - p.p_last0)) * p.s_max + f.kb0 / p.chunk_keys;
+              ((int64_t)f.kvh * p.n_last_pairs + (f.pair - p.p_last0)) * p.s_max + f.chunk;
           const int64_t prow = slot * (2 * kTileRows) + x * kTileRows + r;
           float *dst = p.part_o + prow * D;
 #pragma unroll 1
@@ -1151,15 +1249,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
               uint32_t ov[16];
               ptx::tmem_ld16(tO + hb * 64 + c * 16, ov, 0);
               ptx::tmem_wait_ld();
+#if TA_EPI_FMUL2
+              // O / l with packed FMUL2 (half the FMA-pipe issue of the scalar multiplies)
+              const uint64_t inv2 = f2pack(inv, inv);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                uint64_t o2 = u2pack(ov[2 * e], ov[2 * e + 1]);
+                asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(o2) : "l"(inv2));
+                float a0, a1;
+                f2unpack(o2, a0, a1);
+                pk[c * 8 + e] = ptx::pack_bf16(a0, a1);
+              }
+#else
 #pragma unroll
               for (int e = 0; e < 8; ++e)
                 pk[c * 8 + e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv,
                                                __uint_as_float(ov[2 * e + 1]) * inv);
+#endif
             }
             TRACE_EP(40 + hb, kitem);
             // staging buffer free: the previous TMA store has finished reading it
-            if (threadIdx.x == kEpiWarp0 * 32) ptx::bulk_wait_read0();
-            asm volatile("bar.sync 5, 128;" ::: "memory");
+            if (threadIdx.x == kEpiWarp0 * 32) WS(2, ptx::bulk_wait_read0());
+            WS(3, asm volatile("bar.sync 5, 128;" ::: "memory"));
             TRACE_EP(42 + hb, kitem);
 #pragma unroll
             for (int pc = 0; pc < 8; ++pc)
@@ -1205,6 +1316,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         if (lane == 0) ptx::mbar_arrive(&o_free[x]);
       }
     }
+    WS_DUMP(4, lane == 0 && warp == kEpiWarp0);
   }
   if (threadIdx.x == kEpiWarp0 * 32) ptx::bulk_wait0();  // epilogue TMA stores complete
   __syncthreads();
@@ -1248,8 +1360,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Attn
   // rows without output still take part in the block barriers
   bool live = kvh < p.hq / p.group && r < p.group * T && tok < p.n &&
               !(p.last_only && tok < p.n - p.last);
-  const int r1 = min((pair + 1) * p.pair_tokens, p.n) - 1;
-  const int nch = live ? (r1 + 1 + p.chunk_keys - 1) / p.chunk_keys : 0;
+  const int nch = live ? (int)p.span_pieces[(int64_t)kvh * p.n_last_pairs + lp] : 0;
   const int64_t slot0 = ((int64_t)kvh * p.n_last_pairs + lp) * p.s_max;
   float mx = -INFINITY;
   for (int c = sub + W * lane; c < nch; c += 32 * W) mx = fmaxf(mx, p.part_lse[(slot0 + c) * rows + rr]);

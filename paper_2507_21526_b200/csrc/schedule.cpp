@@ -104,56 +104,45 @@ static Item stream_item(const Geometry &g, int kvh, int64_t p) {
   return make_item(kStream, kvh, p, b0, b1);
 }
 
-void plan_chunks(Geometry *g, int num_ctas) {
-  if (g->dense) {
-    g->chunk_keys = 0;
-    g->s_max = 0;
-    return;
+// Level of the Last Q-K water-filling: the smallest integer L such that the CTAs, each
+// taking floor((L - load_c - kItemOverhead) / 128) blocks, hold all `nblocks` blocks.
+static int64_t fill_level(const std::vector<int64_t> &load, int64_t nblocks) {
+  auto cap = [&](int64_t L) {
+    int64_t t = 0;
+    for (int64_t x : load) t += std::max<int64_t>(0, (L - x - kItemOverhead) / kBlockKeys);
+    return t;
+  };
+  int64_t lo = 0, hi = *std::max_element(load.begin(), load.end()) + kItemOverhead + kBlockKeys * nblocks;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (cap(mid) >= nblocks)
+      hi = mid;
+    else
+      lo = mid + 1;
   }
-  int64_t ctot = 0;
-  if (!g->last_only)
-    for (int64_t p = 0; p < g->p_last0; ++p) ctot += item_cost(*g, stream_item(*g, 0, p));
-  for (int64_t p = g->p_last0; p < g->num_pairs; ++p) {
-    int64_t r0, r1;
-    pair_rows(*g, p, &r0, &r1);
-    ctot += item_cost(*g, make_item(kLastQ, 0, p, 0, r1 + 1));
-  }
-  ctot *= g->hkv;
-  const int64_t div = g->last_only ? kChunkDivLastRows : kChunkDiv;
-  int64_t target = ctot / (div * (int64_t)std::max(1, num_ctas));
-  int64_t ck = 512;
-  while (ck * 2 <= target && ck * 2 <= 16384) ck *= 2;
-  g->chunk_keys = (int)ck;
-  g->s_max = (int)((g->n + ck - 1) / ck);
+  return lo;
 }
 
 Schedule build_schedule(const Geometry &g0, int num_ctas) {
   Schedule s;
   s.g = g0;
-  plan_chunks(&s.g, num_ctas);
-  const Geometry &g = s.g;
+  Geometry &g = s.g;
+  g.chunk_keys = 0;  // variable pieces (schedule version 2)
+  g.s_max = 0;
   s.num_ctas = num_ctas;
 
-  // Canonical order: LASTQ (kvh, pair, chunk), then STREAM or DENSE (kvh, pair).
+  // 1. STREAM (triangle) or DENSE items, canonical order (kvh, pair), by LPT.
   std::vector<Item> canon;
-  if (!g.dense) {
-    for (int kvh = 0; kvh < g.hkv; ++kvh)
-      for (int64_t p = g.p_last0; p < g.num_pairs; ++p) {
-        int64_t r0, r1;
-        pair_rows(g, p, &r0, &r1);
-        for (int64_t kb = 0; kb < r1 + 1; kb += g.chunk_keys)
-          canon.push_back(make_item(kLastQ, kvh, p, kb, std::min<int64_t>(kb + g.chunk_keys, r1 + 1)));
-      }
-    if (!g.last_only)
-      for (int kvh = 0; kvh < g.hkv; ++kvh)
-        for (int64_t p = 0; p < g.p_last0; ++p) canon.push_back(stream_item(g, kvh, p));
-  } else {
+  if (g.dense) {
     for (int kvh = 0; kvh < g.hkv; ++kvh)
       for (int64_t p = 0; p < g.num_pairs; ++p) {
         int64_t r0, r1;
         pair_rows(g, p, &r0, &r1);
         canon.push_back(make_item(kDense, kvh, p, 0, r1 + 1));
       }
+  } else if (!g.last_only) {
+    for (int kvh = 0; kvh < g.hkv; ++kvh)
+      for (int64_t p = 0; p < g.p_last0; ++p) canon.push_back(stream_item(g, kvh, p));
   }
   const size_t ni = canon.size();
   std::vector<int64_t> cost(ni);
@@ -162,23 +151,75 @@ Schedule build_schedule(const Geometry &g0, int num_ctas) {
   std::iota(order.begin(), order.end(), 0u);
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
-
   // LPT: each item to the least-loaded CTA, ties to the lowest CTA id.
   typedef std::pair<int64_t, int> LoadCta;
   std::priority_queue<LoadCta, std::vector<LoadCta>, std::greater<LoadCta>> heap;
   for (int c = 0; c < num_ctas; ++c) heap.push(LoadCta(0, c));
-  std::vector<std::vector<uint32_t>> per(num_ctas);
+  std::vector<std::vector<Item>> per(num_ctas);
+  std::vector<int64_t> load(num_ctas, 0);
   for (uint32_t idx : order) {
     LoadCta top = heap.top();
     heap.pop();
-    per[top.second].push_back(idx);
-    heap.push(LoadCta(top.first + cost[idx], top.second));
+    per[top.second].push_back(canon[idx]);
+    load[top.second] = top.first + cost[idx];
+    heap.push(LoadCta(load[top.second], top.second));
+  }
+
+  // 2. Water-filling of the Last Q-K work (Algorithm 1's split-K "last rows" programs,
+  // P:L622-638; reading R7): the key spans [0, r1+1) of the last pairs, canonical order
+  // (kvh, pair), in 128-key blocks, go to the CTAs in ascending (load, id) order, each up
+  // to the common level; a take is cut at span ends into LASTQ pieces whose chunk index
+  // (Item::pad) is their ordinal within the span.
+  if (!g.dense && g.n_last_pairs > 0) {
+    struct Span { int kvh; int64_t pair, keys, nblk; };
+    std::vector<Span> spans;
+    int64_t total = 0;
+    for (int kvh = 0; kvh < g.hkv; ++kvh)
+      for (int64_t p = g.p_last0; p < g.num_pairs; ++p) {
+        int64_t r0, r1;
+        pair_rows(g, p, &r0, &r1);
+        const int64_t nb = (r1 + 1 + kBlockKeys - 1) / kBlockKeys;
+        spans.push_back(Span{kvh, p, r1 + 1, nb});
+        total += nb;
+      }
+    const int64_t L = fill_level(load, total);
+    std::vector<int> cta(num_ctas);
+    std::iota(cta.begin(), cta.end(), 0);
+    std::stable_sort(cta.begin(), cta.end(), [&](int a, int b) { return load[a] < load[b]; });
+    std::vector<int> pieces(spans.size(), 0);
+    size_t si = 0;
+    int64_t off = 0, rem = total;
+    for (int c : cta) {
+      if (rem == 0) break;
+      int64_t take = std::min(rem, std::max<int64_t>(0, (L - load[c] - kItemOverhead) / kBlockKeys));
+      while (take > 0) {
+        const Span &sp = spans[si];
+        const int64_t k = std::min(take, sp.nblk - off);
+        Item it = make_item(kLastQ, sp.kvh, sp.pair, off * kBlockKeys,
+                            std::min<int64_t>((off + k) * kBlockKeys, sp.keys));
+        it.pad = (uint8_t)pieces[si]++;
+        per[c].push_back(it);
+        load[c] += item_cost(g, it);
+        off += k;
+        take -= k;
+        rem -= k;
+        if (off == sp.nblk) {
+          ++si;
+          off = 0;
+        }
+      }
+    }
+    g.s_max = *std::max_element(pieces.begin(), pieces.end());
+    s.span_pieces.assign(pieces.begin(), pieces.end());
   }
   s.offsets.assign(num_ctas + 1, 0);
-  s.items.reserve(ni);
+  s.items.reserve(ni + (size_t)num_ctas);
   for (int c = 0; c < num_ctas; ++c) {
     s.offsets[c] = (uint32_t)s.items.size();
-    for (uint32_t idx : per[c]) s.items.push_back(canon[idx]);
+#ifdef TA_LASTQ_FIRST  // (experiment) a CTA's LASTQ pieces before its STREAM items
+    std::stable_partition(per[c].begin(), per[c].end(), [](const Item &it) { return it.kind == kLastQ; });
+#endif
+    s.items.insert(s.items.end(), per[c].begin(), per[c].end());
   }
   s.offsets[num_ctas] = (uint32_t)s.items.size();
   return s;
@@ -213,7 +254,7 @@ std::vector<uint8_t> serialize(const Schedule &s) {
 }
 
 int64_t num_partial_slots(const Geometry &g) {
-  return g.dense ? 0 : (int64_t)g.hkv * g.n_last_pairs * g.s_max;
+  return g.dense ? 0 : (int64_t)g.hkv * g.n_last_pairs * g.s_max;  // s_max from build_schedule
 }
 
 size_t workspace_bytes(const Geometry &g) {

@@ -18,11 +18,11 @@ enum ItemKind : uint8_t { kStream = 0, kLastQ = 1, kDense = 2 };
 
 // One unit of work: NQT consecutive packed Q tiles ("a pair") of one kv head and
 // a key range.  STREAM: [key_begin,key_end) is the sliding-window band, the sink
-// [0, min(si, r1+1)) is implicit.  LASTQ: one split-K chunk of [0, r1+1).
-// DENSE: [0, r1+1).
+// [0, min(si, r1+1)) is implicit.  LASTQ: one split-K piece of [0, r1+1); `pad` is its
+// chunk index (ordinal within the pair's span, < 256).  DENSE: [0, r1+1).
 struct Item {
   uint8_t kind;
-  uint8_t pad;
+  uint8_t pad;  // LASTQ: chunk index; else 0
   uint16_t kv_head;
   uint32_t pair;
   uint32_t key_begin;
@@ -40,17 +40,10 @@ constexpr int kSinkRows = 16;       // sink keys folded into a STREAM item's fir
 #ifndef TA_ITEM_OVERHEAD  // (overridable for schedule-policy experiments only; the oracle's
 #define TA_ITEM_OVERHEAD 192  // schedule_ref.py mirrors the defaults)
 #endif
-#ifndef TA_CK_DIV
-#define TA_CK_DIV 8
-#endif
 constexpr int kItemOverhead = TA_ITEM_OVERHEAD;
-// chunk_keys target: C_tot / (div * num_ctas); div = kChunkDiv for triangle layers,
-// kChunkDivLastRows for the final-layer last-rows mode (LASTQ items only: finer chunks
-// there only add items and merge work, measured +10 % cycles at C3 with 8)
-constexpr int kChunkDiv = TA_CK_DIV;
-constexpr int kChunkDivLastRows = 4;
 constexpr uint32_t kScheduleMagic = 0x43534154u;  // "TASC"
-constexpr uint32_t kScheduleVersion = 1;
+constexpr uint32_t kScheduleVersion = 2;          // v2: water-filled variable LASTQ pieces
+constexpr int kMaxCtas = 255;                     // chunk indices are u8 (<= 1 piece per CTA and span)
 
 struct Geometry {
   int64_t n = 0;
@@ -64,8 +57,8 @@ struct Geometry {
   int64_t num_pairs = 0;     // ceil(N / P)
   int64_t p_last0 = 0;       // first pair containing a row >= N - last (num_pairs if none)
   int64_t n_last_pairs = 0;  // num_pairs - p_last0 (triangle), 0 for dense
-  int chunk_keys = 0;        // split-K chunk length for LASTQ items
-  int s_max = 0;             // max chunks per last pair = ceil(N / chunk_keys)
+  int chunk_keys = 0;        // 0: LASTQ pieces have variable length (schedule v2)
+  int s_max = 0;             // max pieces per last pair (set by build_schedule)
 };
 
 struct Schedule {
@@ -73,10 +66,11 @@ struct Schedule {
   int num_ctas = 0;
   std::vector<uint32_t> offsets;  // num_ctas + 1
   std::vector<Item> items;        // per-CTA lists, execution order
+  std::vector<uint8_t> span_pieces;  // LASTQ pieces per (kvh, last pair), [hkv][n_last_pairs]
 };
 
 // Fills the geometry fields that do not depend on num_ctas. Returns false on bad input.
-// chunk_keys / s_max are set by plan_chunks() (they depend on num_ctas).
+// s_max is set by build_schedule() (it depends on num_ctas and the LPT loads).
 // last_only: final-layer mode, only LASTQ items over the last `last` rows (si, sl unused).
 bool make_geometry(int64_t n, int hq, int hkv, int d, bool dense, int si, int sl, int last,
                    Geometry *g, std::string *err, bool last_only = false);
@@ -84,13 +78,11 @@ bool make_geometry(int64_t n, int hq, int hkv, int d, bool dense, int si, int sl
 void pair_rows(const Geometry &g, int64_t p, int64_t *r0, int64_t *r1);
 // Sum of 16-rounded block widths over the item's key blocks + kItemOverhead.
 int64_t item_cost(const Geometry &g, const Item &it);
-// chunk_keys = largest power of two <= C_tot / (4 num_ctas), clamped to [512, 16384],
-// where C_tot is the total cost with every last pair as one unsplit LASTQ item.
-void plan_chunks(Geometry *g, int num_ctas);
-// plan_chunks + enumerate + LPT. num_ctas >= 1.
+// Enumerate + LPT of STREAM/DENSE items + water-filling of the LASTQ work (DESIGN.md
+// section 4).  1 <= num_ctas <= kMaxCtas.
 Schedule build_schedule(const Geometry &g, int num_ctas);
 std::vector<uint8_t> serialize(const Schedule &s);
-// Partial-output slots (split-K workspace) and their byte size.
+// Partial-output slots (split-K workspace) and their byte size (g from build_schedule).
 int64_t num_partial_slots(const Geometry &g);
 size_t workspace_bytes(const Geometry &g);
 

@@ -72,8 +72,8 @@ def test_schedule_per_shard_is_a_kv_head_slice():
     from oracle import schedule_ref
     _, _, items_full = schedule_ref.parse(ta.schedule_export(4096, 32, 8, 128, 148))
     _, _, items_shard = schedule_ref.parse(ta.schedule_export(4096, 4, 1, 128, 148))
-    stream_full = sorted((p, kb, ke) for kind, kvh, p, kb, ke in items_full if kvh == 0 and kind == 0)
-    stream_shard = sorted((p, kb, ke) for kind, kvh, p, kb, ke in items_shard if kind == 0)
+    stream_full = sorted((p, kb, ke) for kind, kvh, p, kb, ke, _ in items_full if kvh == 0 and kind == 0)
+    stream_shard = sorted((p, kb, ke) for kind, kvh, p, kb, ke, _ in items_shard if kind == 0)
     assert stream_full == stream_shard
 
 

@@ -44,7 +44,7 @@ def test_schedule_is_deterministic():
 
 def _block_keeps(geo, item, block, i):
     """Keys of one block that the kernel keeps for row i (DESIGN.md section 4.3 rule)."""
-    kind, kvh, p, kb0, ke0 = item
+    kind, kvh, p, kb0, ke0 = item[:5]
     btype, kb, w = block
     si, sl, last, n = geo["si"], geo["sl"], geo["last"], geo["n"]
     keys = range(kb, kb + w)
@@ -85,11 +85,50 @@ def test_items_cover_mask_exactly_once(seed):
     assert np.array_equal(hits, want.astype(np.int32))
 
 
-def test_lpt_balance_at_paper_configs():
-    for n, hq, hkv, nc, bound in [(32768, 32, 8, 148, 1.05), (131072, 32, 8, 148, 1.01),
-                                  (131072, 4, 1, 148, 1.05)]:
-        geo, ck, s_max, per, load = schedule_ref.schedule(n, hq, hkv, 128, 8, 512, 128, False, nc)
-        assert max(load) / (sum(load) / nc) <= bound, (n, hq, max(load) / (sum(load) / nc))
+@pytest.mark.parametrize("n,hq,hkv,bound", [
+    (32768, 32, 8, 1.02), (131072, 32, 8, 1.01),          # 1 GPU
+    (131072, 4, 1, 1.05), (65536, 4, 1, 1.05),            # Llama, one kv head (8-way shard)
+    (131072, 3, 1, 1.05), (131072, 4, 1, 1.05),           # Qwen at 8 GPUs: 3 + 4 q-head split
+    (65536, 3, 1, 1.05), (131072, 28, 4, 1.01),
+    (32768, 8, 2, 1.05), (32768, 16, 4, 1.05),            # C2 at 4 / 2 GPUs
+])
+def test_lpt_balance_at_paper_configs(n, hq, hkv, bound):
+    geo, ck, s_max, per, load = schedule_ref.schedule(n, hq, hkv, 128, 8, 512, 128, False, 148)
+    assert max(load) / (sum(load) / 148) <= bound, (n, hq, max(load) / (sum(load) / 148))
+
+
+def test_lpt_c2_eight_way_shard_at_stream_granularity():
+    """C2 on an 8-way kv-head shard (N = 32768, 4 q heads): 510 equal STREAM items on 148
+    CTAs force 66 CTAs to hold 4 of them; the Last Q-K work is water-filled into the
+    others, whose pieces cost at least one 128-key block + the 192-column item overhead.
+    The result is within one minimal piece of the 4-item floor (max / mean 1.06; the
+    round-1 fixed-chunk LPT gave 1.14)."""
+    geo, ck, s_max, per, load = schedule_ref.schedule(32768, 4, 1, 128, 8, 512, 128, False, 148)
+    n_stream = sum(1 for lst in per for it in lst if it[0] == schedule_ref.STREAM)
+    stream_cost = schedule_ref.cost(geo, schedule_ref.stream_item(geo, 0, 10))
+    floor = -(-n_stream // 148) * stream_cost
+    assert max(load) <= floor + 2 * schedule_ref.ITEM_OVERHEAD + 128 - 16
+    assert max(load) / (sum(load) / 148) <= 1.065
+
+
+@pytest.mark.parametrize("n,hq,hkv,nc", [(32768, 32, 8, 148), (32768, 4, 1, 148), (4097, 28, 4, 148),
+                                         (1000, 8, 2, 7), (131072, 4, 1, 148)])
+def test_lastq_pieces_tile_each_span_in_order(n, hq, hkv, nc):
+    """Water-filled LASTQ pieces: per (kv head, last pair) they tile [0, r1+1) exactly, in key
+    order, with chunk indices 0..k-1 (the merge's slots); s_max = the largest k."""
+    geo, ck, s_max, per, load = schedule_ref.schedule(n, hq, hkv, 128, 8, 512, 128, False, nc)
+    spans = {}
+    for lst in per:
+        for it in lst:
+            if it[0] == schedule_ref.LASTQ:
+                spans.setdefault((it[1], it[2]), []).append(it)
+    assert s_max == max(len(v) for v in spans.values())
+    for (kvh, p), its in spans.items():
+        its.sort(key=lambda t: t[5])
+        assert [t[5] for t in its] == list(range(len(its)))
+        assert its[0][3] == 0 and its[-1][4] == schedule_ref.rows(geo, p)[1] + 1
+        for a, b in zip(its, its[1:]):
+            assert a[4] == b[3] and a[3] % 128 == 0
 
 
 def test_last_rows_go_through_split_k():
@@ -99,7 +138,7 @@ def test_last_rows_go_through_split_k():
     for i in range(32768 - 128, 32768):
         assert i // geo["P"] in last_pairs
     hdr, off, items = schedule_ref.parse(ta.schedule_export(32768, 32, 8, 128, 148))
-    assert hdr[0] == schedule_ref.MAGIC and hdr[12] == ck and hdr[15] == s_max
+    assert hdr[0] == schedule_ref.MAGIC and hdr[1] == 2 and hdr[12] == 0 and hdr[15] == s_max
 
 
 LAST_ROWS_CASES = [
