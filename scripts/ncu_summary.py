@@ -38,10 +38,10 @@ dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
 dur = num("gpu__time_duration.sum")
 summary = {"tag": tag, "kernel": "attn_kernel<128>", "source": os.path.basename(rep),
            "command": "ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 3 -c 1 "
-                      "python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-dense --no-e2e",
+                      "python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-dense --no-e2e --no-points",
            "dram_bytes_per_launch": dram, "duration_s_under_ncu": dur, "metrics": out}
 os.makedirs(os.path.join(root, "profiles"), exist_ok=True)
 json.dump(summary, open(os.path.join(root, "profiles", f"{tag}_ncu_attn_full.json"), "w"), indent=1)
-json.dump({"dram_bytes_per_launch": dram, "from": f"profiles/{tag}_ncu_attn_full.json"},
+json.dump({"dram_bytes_per_launch": dram, "source": f"profiles/{tag}_ncu_attn_full.json (ncu --set full, round {tag})"},
           open(os.path.join(root, "profiles", "ncu_attn_summary.json"), "w"), indent=1)
 print(json.dumps(summary, indent=1))

@@ -15,7 +15,7 @@ ki, vi, mi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Na
 ls = [(r[ki], float(r[vi].replace(",", "")) / 1000) for r in rows[hi + 1:]
       if len(r) > vi and r[mi] == "gpu__time_duration.sum"]
 out = ["ncu --metrics gpu__time_duration.sum --clock-control none --csv (launch list of: "
-       "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e)",
+       "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-points)",
        "cold-cache, serialised per-launch times: compare shares, not absolutes.", "",
        "per launch (us), in order:"]
 out += [f"  {n[:48]:48s} {t:10.1f}" for n, t in ls]
