@@ -439,6 +439,34 @@ def main():
     merge_ms = max_over_ranks(prof["merge_ms"] / max(1, prof["merge_launches"]))
     gpu_launches = prof["attn_launches"] + prof["merge_launches"]
 
+    # ---- PDL: the same step with the merge launched without programmatic dependent launch
+    # (outer events only, no per-kernel events between the two launches)
+    pdl = None
+    if world == 1 and not args.no_points:
+        def step_ms(n):
+            evs = []
+            barrier()
+            for _ in range(n):
+                if args.l2 == "flush":
+                    flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                layer()
+                b.record(stream)
+                evs.append((a, b))
+            barrier()
+            return statistics.median(a.elapsed_time(b) for a, b in evs)
+        on, off = [], []
+        for _ in range(3):   # interleaved
+            on.append(step_ms(10))
+            ta.set_pdl(False)
+            off.append(step_ms(10))
+            ta.set_pdl(True)
+        pdl = {"step_ms_pdl": statistics.median(on), "step_ms_no_pdl": statistics.median(off),
+               "saved_us": 1e3 * (statistics.median(off) - statistics.median(on)),
+               "what": "median step (attention + merge) with the merge launched with / without "
+                       "programmatic dependent launch, interleaved"}
+
     fl_layer = kept_flops(c, c.hq)
     fl_rank = kept_flops(c, hq_l)
     value = fl_layer / (ms_tri * 1e-3) / 1e12
@@ -646,6 +674,8 @@ def main():
             line["points"] = sweep
         if shard_pts is not None:
             line["shard_points"] = shard_pts
+        if pdl is not None:
+            line["pdl"] = pdl
         if extras is not None:
             line["next_rows"] = extras
         print(json.dumps(line), flush=True)

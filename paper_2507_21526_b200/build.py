@@ -65,11 +65,36 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, defin
         cmd.insert(1, "-DTA_TRACE")
     for d in defines:
         cmd.insert(1, "-D" + d)
+    cmd.insert(1, "-Xptxas=-v")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise subprocess.CalledProcessError(r.returncode, cmd)
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
+        sys.stderr.write(r.stderr)
+    spills = _attn_spills(r.stderr)
+    hot = [x for x in spills if "attn_kernelILi128ELi0E" in x]
+    if hot and so == SO:
+        # A spill in the hot instantiation put local-memory loads on the MMA issue path
+        # (measured: tcgen05.mma groups waited on an LDL of the TMEM base); refuse it.
+        raise RuntimeError("attn_kernel<128, single output> spills registers: " + "; ".join(hot))
+    for x in spills:
+        if x not in hot:
+            sys.stderr.write("warning: " + x + "\n")
     os.replace(so + ".tmp", so)
     return so
+
+
+def _attn_spills(ptxas_log: str):
+    """ptxas -v lines reporting spills for the attention kernel instantiations."""
+    out, cur = [], None
+    for ln in ptxas_log.splitlines():
+        if "Function properties for" in ln:
+            cur = ln.split("for", 1)[1].strip()
+        elif "spill" in ln and cur and "attn_kernel" in cur:
+            if "0 bytes spill stores, 0 bytes spill loads" not in ln:
+                out.append(f"{cur}: {ln.strip()}")
+    return out
 
 
 if __name__ == "__main__":

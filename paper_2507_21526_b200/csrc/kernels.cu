@@ -215,11 +215,12 @@ constexpr bool kPingPong = TA_PINGPONG != 0;
 #define TA_DELAY_TMA 0
 #endif
 // Wait accounting (TA_WAITSTAT builds, with TA_CTA_CLOCK): each role sums the SM cycles it
-// spends in each barrier wait; written at the end to trace[4096 + 64 cta + 8 role + k]
+// spends in each barrier wait (and the MMA issuer in its issue loops); written at the end
+// to trace[4096 + 128 cta + 16 role + k]
 // (roles: 0 TMA producer, 1 MMA issuer, 2/3 softmax tile A/B (warp quarter 0, lane 0),
 // 4 epilogue (warp 0, lane 0)); scripts/waitstat.py prints them.
 #ifdef TA_WAITSTAT
-#define WS_DECL long long ws_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define WS_DECL long long ws_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
 #define WS(k, ...)                          \
   do {                                      \
     const long long ws_t0_ = clock64();     \
@@ -229,7 +230,7 @@ constexpr bool kPingPong = TA_PINGPONG != 0;
 #define WS_DUMP(role, cond)                                                          \
   do {                                                                              \
     if (cond)                                                                       \
-      for (int k_ = 0; k_ < 8; ++k_) p.trace[4096 + 64 * blockIdx.x + 8 * (role) + k_] = ws_acc[k_]; \
+      for (int k_ = 0; k_ < 16; ++k_) p.trace[4096 + 128 * blockIdx.x + 16 * (role) + k_] = ws_acc[k_]; \
   } while (0)
 #else
 #define WS_DECL
@@ -319,7 +320,7 @@ struct ItemStream {
     if (TA_ITEM_PREFETCH && beg < e) nxt = item_at(p, beg);
   }
   __device__ __forceinline__ Item take(const AttnParams &p, uint32_t ii) {
-    if (!TA_ITEM_PREFETCH) return item_at(p, ii);
+    if (!TA_ITEM_PREFETCH) return p.items[ii];
     const Item cur = nxt;
     if (ii + 1 < end) nxt = item_at(p, ii + 1);
     return cur;
@@ -652,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         item_info(p, is.take(p, ii), f);
         if (leader && ii + 1 < it_end) {
           ItemInfo fn;
-          item_info(p, TA_ITEM_PREFETCH ? is.nxt : item_at(p, ii + 1), fn);
+          item_info(p, TA_ITEM_PREFETCH ? is.nxt : p.items[ii + 1], fn);
           for (int x = 0; x < 2; ++x)
             for (int h = 0; h < C::kHalves; ++h)
               ptx::tma_prefetch_l2_3d(&p.tm_q, h * 64, fn.r0 + x * p.tile_tokens, fn.kvh * p.group);
@@ -742,11 +743,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ring_pos(seq, C::kStages, kslot, kph);
         MMA_WAIT(&kv_full[kslot], kph);
         ptx::tc_fence_after();
-        issue_qk(0, kslot, f, b);
-        commit(&s_full[0]);
-        issue_qk(1, kslot, f, b);
-        commit(&s_full[1]);
-        commit(&kv_empty[kslot]);
+        WS(8, issue_qk(0, kslot, f, b));
+        WS(10, commit(&s_full[0]));
+        WS(8, issue_qk(1, kslot, f, b));
+        WS(10, commit(&s_full[1]));
+        WS(10, commit(&kv_empty[kslot]));
         if (f.nb == 1) commit(q_empty);  // Q tiles are free after the item's last QK^T
         while (true) {
           opaque_bases();
@@ -761,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           ItemInfo f1 = f;
           int j1 = j + 1;
           if (last && more) {
-            item_info(p, is.take(p, ii + 1), f1);
+            WS(11, item_info(p, is.take(p, ii + 1), f1));
             j1 = 0;
           }
           Blk b1 = b;
@@ -784,8 +785,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(10, j);
           const uint32_t kitem = ii - it_beg;  // item of block j
           if (j == 0 && kitem > 0) WS(5, MMA_WAIT(&o_free[0], (kitem - 1) & 1u));  // O_A drained
+#ifdef TA_WAITSTAT
+          if (j == 0) ++ws_acc[15];  // items
+          ++ws_acc[14];              // block pairs
+#endif
           if (TA_PV_SPLIT) {
-            issue_pv(0, vslot, f, b, j > 0, 0);  // keys 0..63 while the softmax finishes 64..127
+            WS(9, issue_pv(0, vslot, f, b, j > 0, 0));  // keys 0..63 while the softmax finishes 64..127
             WS(4, MMA_WAIT(&p_hi[0], pph[0] ^ 1u));
           } else {
             MMA_WAIT(&p_hi[0], pph[0]);
@@ -793,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           ptx::tc_fence_after();
           if (!TA_PV_SPLIT) issue_pv(0, vslot, f, b, j > 0, 0);
-          issue_pv(0, vslot, f, b, j > 0, 4);
+          WS(9, issue_pv(0, vslot, f, b, j > 0, 4));
           TRACE_MM(11, j);
           if (last) commit(&o_full[0]);
           if (more) {
@@ -806,8 +811,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             if (!TA_EARLY_K) WS(2, MMA_WAIT(&kv_full[kslot1], kph1));
             ptx::tc_fence_after();
             TRACE_MM(19, j);
-            issue_qk(0, kslot1, f1, b1);
-            commit(&s_full[0]);
+            WS(8, issue_qk(0, kslot1, f1, b1));
+            WS(10, commit(&s_full[0]));
             TRACE_MM(12, j);
           }
           // ---- tile B: PV_B(j), then QK_B(next)
@@ -820,7 +825,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(13, j);
           if (j == 0 && kitem > 0) WS(5, MMA_WAIT(&o_free[1], (kitem - 1) & 1u));  // O_B drained
           if (TA_PV_SPLIT) {
-            issue_pv(1, vslot, f, b, j > 0, 0);  // keys 0..63 while the softmax finishes 64..127
+            WS(9, issue_pv(1, vslot, f, b, j > 0, 0));  // keys 0..63 while the softmax finishes 64..127
             WS(7, MMA_WAIT(&p_hi[1], pph[1] ^ 1u));
           } else {
             MMA_WAIT(&p_hi[1], pph[1]);
@@ -828,16 +833,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           ptx::tc_fence_after();
           if (!TA_PV_SPLIT) issue_pv(1, vslot, f, b, j > 0, 0);
-          issue_pv(1, vslot, f, b, j > 0, 4);
+          WS(9, issue_pv(1, vslot, f, b, j > 0, 4));
           TRACE_MM(14, j);
           if (last) commit(&o_full[1]);
-          commit(&kv_empty[vslot]);
+          WS(10, commit(&kv_empty[vslot]));
           seq += 2;
           if (!more) break;
-          issue_qk(1, kslot1, f1, b1);
-          commit(&s_full[1]);
+          WS(8, issue_qk(1, kslot1, f1, b1));
+          WS(10, commit(&s_full[1]));
           TRACE_MM(15, j);
-          commit(&kv_empty[kslot1]);
+          WS(10, commit(&kv_empty[kslot1]));
           if (j1 + 1 == f1.nb) commit(q_empty);  // last QK^T of that item issued
           if (last) ++ii;
           f = f1;
