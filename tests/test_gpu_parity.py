@@ -231,6 +231,28 @@ def test_full_size_sampled_rows(name):
     assert np.abs(lse[:, rows].double().numpy() - lse_ref).max() < 2e-3
 
 
+@pytest.mark.parametrize("n,hq,hkv", [(32768, 4, 1), (131072, 4, 1), (131072, 3, 1)])
+def test_shard_shapes_sampled_rows(n, hq, hkv):
+    """Per-rank shapes of the 8-GPU kv-head / q-head shards: one kv head,
+    4 (Llama) or 3 (Qwen 3 + 4 split) q heads.  Here the water-filled Last Q-K work splits
+    each last pair's span into 60-150 pieces, so the merge runs its 8-warps-per-row path."""
+    q, k, v = synth.make_qkv(hq, hkv, n, 128, seed=n + hq, dist="iid", si=8)
+    o, lse = _run(q, k, v, 8, 512, 128, False, lse=True)
+    hdr, _, items = schedule_ref_parse(n, hq, hkv)
+    assert hdr[15] > 32, hdr[15]   # s_max: the W = 8 merge
+    rows = _sample_rows(n, 128, np.random.default_rng(2))
+    o_ref, lse_ref, _ = cref.attention(q, k, v, 8, 512, 128, False, rows=rows)
+    _compare(o[:, rows], o_ref, f"shard n{n} hq{hq}")
+    assert np.abs(lse[:, rows].double().numpy() - lse_ref).max() < 2e-3
+
+
+def schedule_ref_parse(n, hq, hkv):
+    from oracle import schedule_ref
+    import torch as _t
+    sms = _t.cuda.get_device_properties(0).multi_processor_count
+    return schedule_ref.parse(ta.schedule_export(n, hq, hkv, 128, min(sms, 255)))
+
+
 def _dense_sample_rows(n, rng):
     rows = set(range(0, 64)) | set(range(n - 32, n)) | set(range(n // 2 - 8, n // 2 + 8))
     rows |= set(rng.choice(n, 96, replace=False).tolist())
