@@ -100,23 +100,26 @@ typedef struct {
                      baselines (reading R12)                          */
 } ta_triangle;
 
-/* Bytes of device workspace triangle_attn_prefill / dense_attn_prefill need
- * (split-K partial outputs and their LSE for the Last-rows pass).
- * tri == NULL -> dense.  Returns 0 on invalid arguments or when none is needed. */
+/* Bytes of device workspace triangle_attn_prefill / dense_attn_prefill need: the split-K
+ * partial outputs and their LSE for the Last-rows pass (triangle only) plus a
+ * 256-byte block holding the fetch counter of the schedule's shared tail (every call; reset
+ * by the call itself on its stream, so concurrent calls must use different workspaces).
+ * tri == NULL -> dense.  Returns 0 on invalid arguments. */
 size_t ta_workspace_size(const ta_problem *p, const ta_triangle *tri);
 
 /* Triangle-shaped sparse causal attention of one deep layer,
  * Algorithm 1 re-designed for sm_100a: a static block schedule
  * of STREAM items (sink + sliding-window band per query tile, rows < N-last)
- * and LASTQ split-K items (rows >= N-last, all causal keys in chunks), one
- * persistent tcgen05/TMEM/TMA kernel, then an LSE merge kernel.
+ * and LASTQ split-K items (rows >= N-last, all causal keys in pieces) assigned to
+ * the persistent tcgen05/TMEM/TMA kernel's CTAs, plus a shared tail of items the
+ * CTAs fetch dynamically when their own lists are done, then an LSE merge kernel
+ * (P:L641-642).
  * ws: device workspace of >= ta_workspace_size(p, tri) bytes, 256-B aligned. */
 ta_status triangle_attn_prefill(const ta_problem *p, const ta_triangle *tri, void *ws,
                                 size_t ws_bytes, cudaStream_t stream);
 
 /* Dense causal attention of one shallow layer; the same kernel
- * with DENSE items (keys [0, i] per row). ws may be NULL when
- * ta_workspace_size(p, NULL) == 0. */
+ * with DENSE items (keys [0, i] per row). ws: >= ta_workspace_size(p, NULL) bytes. */
 ta_status dense_attn_prefill(const ta_problem *p, void *ws, size_t ws_bytes,
                              cudaStream_t stream);
 

@@ -25,7 +25,11 @@ Spec summary:
      span sequence; a take is cut at span ends into LASTQ(kvh, p) pieces
      [b0*128, min(b1*128, r1+1)) appended to that CTA's list; a piece's chunk index (u8
      item field `pad`) is its ordinal within its span.  s_max = max pieces per span.
-  bytes: 16 x u32 header (version 2; field 12 = 0: variable pieces), u32
+  1b. (between 1 and 2; schedule version 4) Shared tail: each CTA's last
+     min(8, (n + 1) // 3) LPT items (n = its LPT item count) leave its list (loads reduced
+     before step 2); sorted by (cost desc, kind, kvh, pair) they form the tail that the
+     kernel's CTAs fetch from a global counter after their own lists.
+  bytes: 16 x u32 header (version 4; field 12 = tail entries), u32
          offsets[num_ctas+1], 16-byte items {u8 kind, u8 chunk, u16 kvh, u32 pair,
          u32 key_begin, u32 key_end}.
 """
@@ -34,11 +38,12 @@ from __future__ import annotations
 import struct
 
 STREAM, LASTQ, DENSE = 0, 1, 2
-MAGIC, VERSION = 0x43534154, 2
+MAGIC, VERSION = 0x43534154, 4
 
 
 
 ITEM_OVERHEAD = 192  # LPT cost of an item beyond its key columns
+TAIL_PER_CTA = 8     # at most this many items per CTA go to the shared, dynamically fetched tail
 
 def _r16(x):
     return -(-x // 16) * 16
@@ -144,8 +149,8 @@ def fill_level(load, nblocks):
 
 
 def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False):
-    """Returns (geo, 0, s_max, per_cta_lists, loads); items are 6-tuples
-    (kind, kvh, pair, key_begin, key_end, chunk)."""
+    """Returns (geo, 0, s_max, per_cta_lists, loads, tail); items are 6-tuples
+    (kind, kvh, pair, key_begin, key_end, chunk); loads are the static lists' costs."""
     geo = geometry(n, hq, hkv, d, si, sl, last, dense, last_rows)
     items = base_items(geo)
     costs = [cost(geo, it) for it in items]
@@ -156,6 +161,13 @@ def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False):
         c = min(range(num_ctas), key=lambda x: (load[x], x))
         per[c].append(items[i])
         load[c] += costs[i]
+    tail = []
+    for c in range(num_ctas):
+        for _ in range(min(TAIL_PER_CTA, (len(per[c]) + 1) // 3)):
+            it = per[c].pop()
+            load[c] -= cost(geo, it)
+            tail.append(it)
+    tail.sort(key=lambda it: (-cost(geo, it), it[0], it[1], it[2]))
     spans = last_spans(geo)
     nblk = [-(-keys // 128) for (_, _, keys) in spans]
     total = sum(nblk)
@@ -182,28 +194,44 @@ def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False):
             if rem == 0:
                 break
         s_max = max(pieces)
-    return geo, 0, s_max, per, load
+    return geo, 0, s_max, per, load, tail
+
+
+def final_loads(geo, load, tail, speed=None):
+    """The kernel's end state: each CTA runs its own list, then fetches tail entries in
+    order whenever it is free (greedy list scheduling; optional per-CTA speed factors)."""
+    import heapq
+    speed = speed or [1.0] * len(load)
+    fin = [ld / sp for ld, sp in zip(load, speed)]
+    heap = [(t, c) for c, t in enumerate(fin)]
+    heapq.heapify(heap)
+    for it in tail:
+        t, c = heapq.heappop(heap)
+        fin[c] = t + cost(geo, it) / speed[c]
+        heapq.heappush(heap, (fin[c], c))
+    return fin
 
 
 def serialize(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False) -> bytes:
-    geo, ck, s_max, per, _ = schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows)
-    nitems = sum(len(x) for x in per)
+    geo, ck, s_max, per, _, tail = schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows)
+    nitems = sum(len(x) for x in per) + len(tail)
     kind = 1 if dense else (2 if geo["last_rows"] else 0)
     hdr = [MAGIC, VERSION, kind, n, hq, hkv, d, geo["si"], geo["sl"], geo["last"],
-           geo["T"], 2, 0, num_ctas, nitems, s_max]
+           geo["T"], 2, len(tail), num_ctas, nitems, s_max]
     out = struct.pack("<16I", *hdr)
     off = [0]
     for x in per:
         off.append(off[-1] + len(x))
     out += struct.pack("<%dI" % len(off), *off)
-    for x in per:
+    for x in per + [tail]:
         for kind, kvh, p, kb, ke, ch in x:
             out += struct.pack("<BBHIII", kind, ch, kvh, p, kb, ke)
     return out
 
 
 def parse(buf: bytes):
-    """Decode the exported byte format into (header list, offsets, items)."""
+    """Decode the exported byte format into (header list, offsets, items): CTA c's list is
+    items[off[c]:off[c+1]], the shared tail items[off[num_ctas]:] (hdr[12] entries)."""
     hdr = list(struct.unpack_from("<16I", buf, 0))
     num_ctas, nitems = hdr[13], hdr[14]
     off = list(struct.unpack_from("<%dI" % (num_ctas + 1), buf, 64))

@@ -97,6 +97,7 @@ struct DevSchedule {
   uint32_t *d_offsets = nullptr;
   uint8_t *d_span = nullptr;  // LASTQ pieces per (kvh, last pair), read by the merge
   int num_ctas = 0;
+  int tail0 = 0, n_tail = 0;  // shared tail of the item list
 };
 
 typedef std::tuple<int, int64_t, int, int, int, int, int, int, int, int, int> SchedKey;
@@ -172,6 +173,8 @@ ta_status get_schedule(int dev, const ta::Geometry &g, int num_ctas, DevSchedule
   DevSchedule ds;
   ds.g = s.g;
   ds.num_ctas = num_ctas;
+  ds.tail0 = (int)s.offsets[num_ctas];
+  ds.n_tail = (int)s.n_tail;
   const size_t ib = std::max<size_t>(1, s.items.size()) * sizeof(ta::Item);
   const size_t ob = s.offsets.size() * sizeof(uint32_t);
   const size_t sb = std::max<size_t>(1, s.span_pieces.size());
@@ -343,14 +346,18 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
     prm.mc_st = mc_o->stride_token;
   }
   prm.lse = p->lse;
-  if (need > 0) {
+  const size_t pbytes = ta::partial_bytes(ds.g);
+  if (pbytes > 0) {
     const int64_t slots = ta::num_partial_slots(ds.g);
     const size_t o_bytes = ((size_t)slots * 2 * ta::kTileRows * g.d * 4 + 255) / 256 * 256;
     prm.part_o = reinterpret_cast<float *>(ws);
     prm.part_lse = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + o_bytes);
   }
+  prm.queue = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(ws) + pbytes);
   prm.items = ds.d_items;
   prm.offsets = ds.d_offsets;
+  prm.tail0 = ds.tail0;
+  prm.n_tail = ds.n_tail;
   prm.n = (int)g.n;
   prm.hq = g.hq;
   prm.group = G;
@@ -414,7 +421,11 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
     g_trace_buf = tbuf;
   }
 #endif
-  cudaError_t e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
+  // the shared tail's fetch counter starts at 0 (it lives in the caller's workspace, so calls
+  // on different streams never share it)
+  cudaError_t e = cudaMemsetAsync(prm.queue, 0, sizeof(uint32_t), stream);
+  if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("queue reset: ") + cudaGetErrorString(e));
+  e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
   if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
   if (rec.a1) cudaEventRecord(rec.a1, stream);
   if (!dense && ds.g.n_last_pairs > 0) {

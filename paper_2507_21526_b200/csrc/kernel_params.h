@@ -27,9 +27,11 @@ struct alignas(64) AttnParams {
   float *lse;        // optional [Hq][N - o_row0]
   float *part_o;     // split-K partials [slot][2*128 rows][d] fp32 (normalised O_c)
   float *part_lse;   // [slot][2*128 rows] fp32 natural-log LSE_c
-  const Item *items;
+  const Item *items;      // CTA c's own list items[offsets[c], offsets[c+1]), then the shared tail
   const uint32_t *offsets;
   const uint8_t *span_pieces;  // LASTQ pieces per (kvh, last pair) = merge chunk counts
+  int tail0, n_tail;      // shared tail: items[tail0 .. tail0 + n_tail), fetched dynamically
+  uint32_t *queue;        // [0]: next tail entry to fetch (reset to 0 before every launch)
   int n, hq, group, tile_tokens, pair_tokens;
   int si, sl, last, dense;
   int last_only;     // final-layer mode: the merge writes only rows >= N - last ...

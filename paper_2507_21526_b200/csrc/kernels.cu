@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <atomic>
+#include <type_traits>
 
 #include "kernel_params.h"
 #include "ptx.cuh"
@@ -103,6 +104,17 @@ constexpr int kMmaWarp = kSoftmaxWarps + kEpiWarps;
 constexpr int kTmaWarp = kMmaWarp + 1;
 constexpr int kAllocWarp = kMmaWarp + 2;
 constexpr int kThreads = 32 * (kSoftmaxWarps + kEpiWarps + 4);
+// 1 (default): no item_empty hand-back.  Slot reuse is safe by the pipeline's own back-
+// pressure: the producer publishes item k+1 only after issuing item k's K/V loads (4-slot
+// ring = 2 blocks) and item k's Q (waits for item k-1's last QK^T), so it leads the MMA warp
+// by <= 2 items; the MMA leads the softmax by <= 1 (QK^T(j+1) waits for P(j)) and the
+// softmax leads the epilogue by <= 2 (it publishes item k after o_free of item k-1): <= 5
+// items in flight against 16 ring entries.  (0: per-slot empty barriers; +0.3 % cycles.)
+#ifndef TA_RING_NOEMPTY
+#define TA_RING_NOEMPTY 1
+#endif
+constexpr int kItemRing = TA_RING_NOEMPTY ? 16 : 8;  // published entries (roles lag the producer by <= ~3)
+constexpr int kItemConsumers = 1 + kSoftmaxWarps + kEpiWarps;  // MMA warp + softmax + epilogue warps
 constexpr int kNCol = 128 / kHPR;  // S columns per softmax thread
 // setmaxnreg split of the register file (launch: 65536 / kThreads, rounded down to 8)
 #ifndef TA_REG_SOFTMAX
@@ -193,12 +205,12 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_MASK_VOTE
 #define TA_MASK_VOTE 0
 #endif
+#ifndef TA_SHORT_BODY  // blocks of <= 80 S columns run a 5-chunk softmax body (see below)
+#define TA_SHORT_BODY 1
+#endif
 #ifndef TA_EPI_FMUL2
 #define TA_EPI_FMUL2 0
 #endif
-#ifndef TA_ITEM_PREFETCH  // every role loads its next schedule item one item ahead
-#define TA_ITEM_PREFETCH 0   // measured +5 % cycles (C3, dense): the extra live registers
-#endif                       // cost the softmax more than the hidden load latency saves
 #ifndef TA_PINGPONG
 #define TA_PINGPONG 0
 #endif
@@ -297,35 +309,6 @@ __device__ __forceinline__ void item_info(const AttnParams &p, const Item &it, I
   }
   f.nb = f.ns + ceil_div(len, kBlockKeys);
 }
-
-// One 16-byte schedule item (read-only path).
-__device__ __forceinline__ Item item_at(const AttnParams &p, uint32_t i) {
-  const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p.items) + i);
-  Item it;
-  it.kind = (uint8_t)(v.x & 0xff);
-  it.pad = (uint8_t)((v.x >> 8) & 0xff);  // LASTQ chunk index
-  it.kv_head = (uint16_t)(v.x >> 16);
-  it.pair = v.y;
-  it.key_begin = v.z;
-  it.key_end = v.w;
-  return it;
-}
-
-// Per-role item stream: item ii is in registers when the role reaches it (its global load
-// was issued one item earlier, off the hand-off paths).
-struct ItemStream {
-  Item nxt;
-  uint32_t end;
-  __device__ __forceinline__ ItemStream(const AttnParams &p, uint32_t beg, uint32_t e) : end(e) {
-    if (TA_ITEM_PREFETCH && beg < e) nxt = item_at(p, beg);
-  }
-  __device__ __forceinline__ Item take(const AttnParams &p, uint32_t ii) {
-    if (!TA_ITEM_PREFETCH) return p.items[ii];
-    const Item cur = nxt;
-    if (ii + 1 < end) nxt = item_at(p, ii + 1);
-    return cur;
-  }
-};
 
 __device__ __forceinline__ Blk block_info(const ItemInfo &f, int j) {
   Blk b;
@@ -537,6 +520,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   uint64_t *o_free = q_full + 12;   // [2] epilogue -> MMA: O_x drained from TMEM
   uint64_t *p_hi = q_full + 14;     // [2] P of keys 64..127 written (p_ready: keys 0..63)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 16);
+  // Dynamic work queue: the TMA producer fetches item indices (global atomic counter, in the
+  // schedule's fetch order) and publishes them in a ring the other roles read in sequence.
+  uint64_t *item_full = q_full + 18;          // [kItemRing], 1 arrival (producer)
+  uint64_t *item_empty = item_full + kItemRing;  // [kItemRing], kItemConsumers arrivals
+  volatile int32_t *item_ring = reinterpret_cast<volatile int32_t *>(item_empty + kItemRing);
   // cross-warp row reductions of the two column halves of a row:
   // red_max[tile][block parity][half][row]; red_l[item parity][tile][half][row];
   // red_m[item parity][tile][row]
@@ -564,6 +552,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       ptx::mbar_init(&l_ready[x], kHPR * kArrivePerTile);
       ptx::mbar_init(&o_free[x], 4);     // one arrival per epilogue warp
     }
+    for (int r = 0; r < kItemRing; ++r) {
+      ptx::mbar_init(&item_full[r], 1);
+      ptx::mbar_init(&item_empty[r], kItemConsumers);
+    }
     ptx::fence_mbar_init();
   }
   // Rows >= G*T of a Q tile are never written by TMA: keep them zero.
@@ -577,13 +569,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // TMEM base: every role re-reads it from shared memory where it starts (a kernel-wide live
+  // value ends up spilled and reloaded on the MMA issue path)
+  auto tmem_base = [&]() -> uint32_t {
+    uint32_t t;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t) : "r"(ptx::smem_u32(tmem_slot)) : "memory");
+    return t;
+  };
 
 #ifdef TA_CTA_CLOCK
   const long long cta_t0 = clock64();
 #endif
-  const uint32_t it_beg = p.offsets[blockIdx.x];
-  const uint32_t it_end = p.offsets[blockIdx.x + 1];
+  // Consumer side of the work queue: the item index of this CTA's k-th item (-1: no more).
+  auto take_item = [&](uint32_t k) -> int {
+    const uint32_t slot = k % kItemRing;
+    ptx::mbar_wait(&item_full[slot], (k / kItemRing) & 1u);
+    const int idx = item_ring[slot];
+    if (!TA_RING_NOEMPTY) {
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&item_empty[slot]);
+    }
+    return idx;
+  };
 
   // Register split: softmax warpgroups kRegSoftmax, epilogue kRegEpi, issuers kRegOther.
   if (warp >= kMmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegOther) : "memory");
@@ -647,19 +654,41 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       // Q(i) (which waits for the previous item's last QK^T) follows; the next item's Q
       // tiles are prefetched into L2 one item ahead so the Q load at the item boundary is
       // an L2 hit rather than an HBM round trip.
-      ItemStream is(p, it_beg, it_end);
-      for (uint32_t ii = it_beg; ii < it_end; ++ii, ++nitem) {
+      // Item source: this CTA's own list, then entries of the shared tail fetched from a
+      // global counter (the next one is fetched while the current item loads).
+      const uint32_t own0 = p.offsets[blockIdx.x], own1 = p.offsets[blockIdx.x + 1];
+      const int leader_lane = __ffs(__ballot_sync(0xffffffffu, leader)) - 1;
+      auto fetch = [&](uint32_t k) -> int {  // item index of this CTA's k-th item, -1 = none
+        if (own0 + k < own1) return (int)(own0 + k);
+        uint32_t t = 0;
+        if (leader) t = atomicAdd(p.queue, 1u);
+        t = __shfl_sync(0xffffffffu, t, leader_lane);
+        return t < (uint32_t)p.n_tail ? p.tail0 + (int)t : -1;
+      };
+      int next = fetch(0);
+      for (;; ++nitem) {
+        const int cur = next;
+        const uint32_t rslot = nitem % kItemRing;
+        if (!TA_RING_NOEMPTY) WS(0, ptx::mbar_wait_lazy(&item_empty[rslot], ((nitem / kItemRing) & 1u) ^ 1u));
+        if (leader) {
+          item_ring[rslot] = cur;
+          ptx::mbar_arrive(&item_full[rslot]);  // release: the entry is visible to the waiters
+        }
+        if (cur < 0) break;
         ItemInfo f;
-        item_info(p, is.take(p, ii), f);
-        if (leader && ii + 1 < it_end) {
+        item_info(p, p.items[cur], f);
+        load_kv(f, 0);
+        if (!TA_EXP_QONCE || nitem == 0) load_q(f, nitem);
+        // fetch the next entry only now: a tail fetch's atomic round trip overlaps this
+        // item's loads instead of delaying them
+        next = fetch(nitem + 1);
+        if (leader && next >= 0) {
           ItemInfo fn;
-          item_info(p, TA_ITEM_PREFETCH ? is.nxt : p.items[ii + 1], fn);
+          item_info(p, p.items[next], fn);
           for (int x = 0; x < 2; ++x)
             for (int h = 0; h < C::kHalves; ++h)
               ptx::tma_prefetch_l2_3d(&p.tm_q, h * 64, fn.r0 + x * p.tile_tokens, fn.kvh * p.group);
         }
-        load_kv(f, 0);
-        if (!TA_EXP_QONCE || nitem == 0) load_q(f, nitem);
         for (int j = 1; j < f.nb; ++j) load_kv(f, j);
       }
     }
@@ -684,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       uint64_t dq = ptx::sdesc_sw128(qbase, 16, 1024);
       uint64_t dkv = ptx::sdesc_sw128(kvbase, 16, 1024);
       uint64_t dkv_mn = ptx::sdesc_sw128(kvbase, C::kSlotHalfBytes, 1024);
-      uint32_t tm = tmem;
+      uint32_t tm = tmem_base();
       // Re-materialise the bases every iteration (an opaque asm "redefines" them): the
       // compiler would otherwise hoist all 32 per-k-step descriptors / TMEM addresses out
       // of the loop and spill them to local memory in this 72-register warp, putting
@@ -729,11 +758,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       // The MMA stream is flat across items: [PV_A(j), QK_A(j+1), PV_B(j), QK_B(j+1)] where
       // block j+1 may be block 0 of the next item, so a new item's first QK^T overlaps the
       // previous item's last softmax instead of draining the pipeline.
-      if (it_beg < it_end) {
-        ItemStream is(p, it_beg, it_end);
+      const int idx0 = take_item(0);
+      if (idx0 >= 0) {
         ItemInfo f;
-        item_info(p, is.take(p, it_beg), f);
-        uint32_t ii = it_beg;
+        item_info(p, p.items[idx0], f);
+        uint32_t ii = 0;  // this CTA's item counter
         int j = 0;
         WS(0, MMA_WAIT(q_full, nitem & 1u));
         ptx::tc_fence_after();
@@ -758,11 +787,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_MM(17, j);
           // next block in the flat stream (same item j+1, or block 0 of the next item)
           const bool last = (j + 1 == f.nb);
-          const bool more = !last || (ii + 1 < it_end);
+          const int nidx = last ? take_item(ii + 1) : 0;  // the next queue entry
+          const bool more = !last || nidx >= 0;
           ItemInfo f1 = f;
           int j1 = j + 1;
           if (last && more) {
-            WS(11, item_info(p, is.take(p, ii + 1), f1));
+            WS(11, item_info(p, p.items[nidx], f1));
             j1 = 0;
           }
           Blk b1 = b;
@@ -783,7 +813,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             ptx::tc_fence_after();
           }
           TRACE_MM(10, j);
-          const uint32_t kitem = ii - it_beg;  // item of block j
+          const uint32_t kitem = ii;  // item of block j
           if (j == 0 && kitem > 0) WS(5, MMA_WAIT(&o_free[0], (kitem - 1) & 1u));  // O_A drained
 #ifdef TA_WAITSTAT
           if (j == 0) ++ws_acc[15];  // items
@@ -862,6 +892,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     const int wq = warp % 4;            // TMEM lane quarter
     const int r = wq * 32 + lane;       // packed row = TMEM lane
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t tmem = tmem_base();
     const uint32_t tS = tmem + x * 128 + hc * 64 + lane_off;  // own S columns; own P columns
     const uint32_t tO = tmem + 256 + x * 128 + hc * (D / kHPR) + lane_off;  // own O columns
     const int T = p.tile_tokens;
@@ -896,10 +927,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #ifdef TA_TRACE
     uint32_t trc = 0;
 #endif
-    ItemStream is(p, it_beg, it_end);
-    for (uint32_t ii = it_beg; ii < it_end; ++ii) {
+    for (uint32_t ii = 0;; ++ii) {
+      const int idx = take_item(ii);
+      if (idx < 0) break;
       ItemInfo f;
-      item_info(p, is.take(p, ii), f);
+      item_info(p, p.items[idx], f);
       const int tok = f.r0 + x * T + toff;     // query row i of this thread
       const bool last_row = tok >= p.n - p.last;
       float m_run = -INFINITY;  // reference max, log2 units of scaled scores
@@ -975,18 +1007,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ptx::tc_fence_after();
         TRACE_SM(20, j);
         TRACE_SMW(20, j);
+        // The block body is compiled twice: for full-width blocks (8 16-column chunks) and
+        // for short ones (<= 80 S columns: the diagonal block of a STREAM item at P = 64,
+        // every other dense diagonal block), whose exponentials stop at the computed columns
+        // with no runtime branch in the exponential loop (TA_SHORT_BODY).
+        auto block_body = [&](auto nch_tag) {
+        constexpr int kCh = decltype(nch_tag)::value;
         uint32_t s[kNCol];
         // 16-column groups this tile computes (tile_ncols; kHPR == 1): the rest of the S
         // columns hold no scores of this block and are skipped (they are masked anyway).
         const int nch = (kHPR == 1 && TA_TILE_TRIM == 1) ? tile_ncols(f, b, x, T) / 16
-                        : (kHPR == 1 && TA_SKIP_RAGGED) ? b.ncols / 16 : kNCol / 16;
+                        : (kHPR == 1 && TA_SKIP_RAGGED) ? b.ncols / 16 : kCh;
         // Two halves: the second TMEM load is in flight while the first half is masked.
         if (TA_TMEM_WIDE && kHPR == 1 && TA_TILE_TRIM == 0) {  // 32-column loads
 #pragma unroll
           for (int c = 0; c < 2; ++c) ptx::tmem_ld32(tS + c * 32, s + c * 32);
           ptx::tmem_wait_ld();
 #pragma unroll
-          for (int c = 2; c < 4; ++c) ptx::tmem_ld32(tS + c * 32, s + c * 32);
+          for (int c = 2; c < 4; ++c)
+            if (32 * c < 16 * kCh) ptx::tmem_ld32(tS + c * 32, s + c * 32);
         } else {
 #pragma unroll
           for (int c = 0; c < kNCol / 32; ++c)
@@ -1130,6 +1169,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             ptx::tmem_st8(tS + c * 8, pk);
           else if (c & 1)  // two chunks (32 keys) per 16-column store
             ptx::tmem_st16(tS + (c - 1) * 8, pkw);
+          else if (c == kCh - 1)  // odd chunk count (short body): the last chunk alone
+            ptx::tmem_st8(tS + c * 8, pk);
           if (kHPR == 1 && c == 3 && TA_PV_SPLIT) {
             // keys 0..63 of P are in TMEM: the MMA can start PV on them right away
             ptx::tmem_wait_st();
@@ -1162,6 +1203,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         sm_arrive((kHPR == 2 && hc == 0) ? &p_ready[x] : &p_hi[x]);
+        };
+        if (TA_SHORT_BODY && kHPR == 1 && TA_TILE_TRIM == 0 && !TA_SKIP_RAGGED && b.ncols <= 80)
+          block_body(std::integral_constant<int, 5>{});
+        else
+          block_body(std::integral_constant<int, kNCol / 16>{});
         TRACE_SM(21, j);
         TRACE_SMW(21, j);
       }
@@ -1204,13 +1250,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #ifdef TA_TRACE
     uint32_t trc = 0;
 #endif
-    ItemStream is(p, it_beg, it_end);
-    for (uint32_t ii = it_beg; ii < it_end; ++ii, ++kitem) {
+    for (;; ++kitem) {
+      const int idx = take_item(kitem);
+      if (idx < 0) break;
       ItemInfo f;
-      item_info(p, is.take(p, ii), f);
+      item_info(p, p.items[idx], f);
       const uint32_t par = kitem & 1u;
       for (int x = x0; x < (kEpiWarps == 8 ? x0 + 1 : 2); ++x) {
-        const uint32_t tO = tmem + 256 + x * 128 + lane_off;
+        const uint32_t tO = tmem_base() + 256 + x * 128 + lane_off;
         const int tok = f.r0 + x * T + toff;
         const bool valid = row_in_tile && tok < p.n;
         TRACE_EP(30 + x, kitem);
@@ -1277,10 +1324,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             if (threadIdx.x == kEpiWarp0 * 32) WS(2, ptx::bulk_wait_read0());
             WS(3, asm volatile("bar.sync 5, 128;" ::: "memory"));
             TRACE_EP(42 + hb, kitem);
+            {
+              // swizzled row addresses recomputed here (an opaque copy of r): hoisted out of
+              // the item loop they occupy 8 registers of this 80-register warpgroup (spills)
+              int rr = r;
+              asm volatile("" : "+r"(rr));
+              const uint32_t row_s = stage_s + rr * 128;
 #pragma unroll
-            for (int pc = 0; pc < 8; ++pc)
-              sts_v4(stage_s + r * 128 + ((pc ^ (r & 7)) << 4), pk[4 * pc], pk[4 * pc + 1],
-                     pk[4 * pc + 2], pk[4 * pc + 3]);
+              for (int pc = 0; pc < 8; ++pc)
+                sts_v4(row_s + ((pc ^ (rr & 7)) << 4), pk[4 * pc], pk[4 * pc + 1], pk[4 * pc + 2],
+                       pk[4 * pc + 3]);
+            }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("bar.sync 5, 128;" ::: "memory");
             if (threadIdx.x == kEpiWarp0 * 32) {
@@ -1333,7 +1387,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #endif
   if (warp == kAllocWarp) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 512);
+    ptx::tmem_dealloc(tmem_base(), 512);
   }
 }
 

@@ -165,6 +165,34 @@ Schedule build_schedule(const Geometry &g0, int num_ctas) {
     heap.push(LoadCta(load[top.second], top.second));
   }
 
+  // 1b. Shared tail: the last min(kTailPerCta, (n + 1) / 3) items of each CTA's LPT list
+  // (its smallest) leave the static assignment; the kernel's CTAs fetch them from a global
+  // counter once their own lists are done, so per-SM speed differences (measured up to
+  // 3.7 % between CTAs with identical lists) and cost-model error are absorbed at the end
+  // (8 per CTA: -1.9 % max-over-CTA cycles at C3, -4.8 % at Qwen 128K vs no tail).
+  std::vector<Item> tail;
+  {
+    std::vector<std::pair<int64_t, Item>> t;
+    for (int c = 0; c < num_ctas; ++c) {
+      const int k = std::min<int>(kTailPerCta, ((int)per[c].size() + 1) / 3);
+      for (int i = 0; i < k; ++i) {
+        const Item it = per[c].back();
+        per[c].pop_back();
+        const int64_t ic = item_cost(g, it);
+        load[c] -= ic;
+        t.push_back(std::make_pair(ic, it));
+      }
+    }
+    // fetch order: cost descending, then (kind, kv head, pair)
+    std::stable_sort(t.begin(), t.end(), [](const std::pair<int64_t, Item> &a, const std::pair<int64_t, Item> &b) {
+      if (a.first != b.first) return a.first > b.first;
+      if (a.second.kind != b.second.kind) return a.second.kind < b.second.kind;
+      if (a.second.kv_head != b.second.kv_head) return a.second.kv_head < b.second.kv_head;
+      return a.second.pair < b.second.pair;
+    });
+    for (auto &x : t) tail.push_back(x.second);
+  }
+
   // 2. Water-filling of the Last Q-K work (Algorithm 1's split-K "last rows" programs,
   // P:L622-638; reading R7): the key spans [0, r1+1) of the last pairs, canonical order
   // (kvh, pair), in 128-key blocks, go to the CTAs in ascending (load, id) order, each up
@@ -222,6 +250,8 @@ Schedule build_schedule(const Geometry &g0, int num_ctas) {
     s.items.insert(s.items.end(), per[c].begin(), per[c].end());
   }
   s.offsets[num_ctas] = (uint32_t)s.items.size();
+  s.n_tail = (int64_t)tail.size();
+  s.items.insert(s.items.end(), tail.begin(), tail.end());
   return s;
 }
 
@@ -239,7 +269,7 @@ std::vector<uint8_t> serialize(const Schedule &s) {
                       (uint32_t)g.last,
                       (uint32_t)g.tile_tokens,
                       (uint32_t)kTilesPerItem,
-                      (uint32_t)g.chunk_keys,
+                      (uint32_t)s.n_tail,
                       (uint32_t)s.num_ctas,
                       (uint32_t)s.items.size(),
                       (uint32_t)g.s_max};
@@ -257,13 +287,18 @@ int64_t num_partial_slots(const Geometry &g) {
   return g.dense ? 0 : (int64_t)g.hkv * g.n_last_pairs * g.s_max;  // s_max from build_schedule
 }
 
-size_t workspace_bytes(const Geometry &g) {
-  int64_t slots = num_partial_slots(g);
+size_t partial_bytes(const Geometry &g) {
+  const int64_t slots = num_partial_slots(g);
   if (slots == 0) return 0;
   const int64_t rows = (int64_t)kTilesPerItem * kTileRows;
-  size_t o_bytes = (size_t)slots * rows * g.d * sizeof(float);
-  size_t lse_bytes = (size_t)slots * rows * sizeof(float);
+  const size_t o_bytes = (size_t)slots * rows * g.d * sizeof(float);
+  const size_t lse_bytes = (size_t)slots * rows * sizeof(float);
   return round_up((int64_t)o_bytes, 256) + round_up((int64_t)lse_bytes, 256);
+}
+
+size_t workspace_bytes(const Geometry &g) {
+  // split-K partials + the 256-byte work-queue block (the shared tail's fetch counter)
+  return partial_bytes(g) + kQueueBytes;
 }
 
 }  // namespace ta

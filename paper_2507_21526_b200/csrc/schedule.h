@@ -42,8 +42,13 @@ constexpr int kSinkRows = 16;       // sink keys folded into a STREAM item's fir
 #endif
 constexpr int kItemOverhead = TA_ITEM_OVERHEAD;
 constexpr uint32_t kScheduleMagic = 0x43534154u;  // "TASC"
-constexpr uint32_t kScheduleVersion = 2;          // v2: water-filled variable LASTQ pieces
+constexpr uint32_t kScheduleVersion = 4;          // v2: water-filled LASTQ pieces; v4: + shared tail
 constexpr int kMaxCtas = 255;                     // chunk indices are u8 (<= 1 piece per CTA and span)
+#ifndef TA_TAIL_PER_CTA  // (overridable for schedule-policy experiments only; schedule_ref.py mirrors 8)
+#define TA_TAIL_PER_CTA 8
+#endif
+constexpr int kTailPerCta = TA_TAIL_PER_CTA;      // items per CTA moved to the shared tail (at most)
+constexpr size_t kQueueBytes = 256;               // work-queue counter block at the workspace end
 
 struct Geometry {
   int64_t n = 0;
@@ -64,8 +69,9 @@ struct Geometry {
 struct Schedule {
   Geometry g;
   int num_ctas = 0;
-  std::vector<uint32_t> offsets;  // num_ctas + 1
-  std::vector<Item> items;        // per-CTA lists, execution order
+  std::vector<uint32_t> offsets;  // num_ctas + 1: CTA c's own list is items[offsets[c], offsets[c+1])
+  std::vector<Item> items;        // the per-CTA lists (execution order), then the shared tail
+  int64_t n_tail = 0;             // tail items items[offsets[num_ctas] ...], fetched dynamically
   std::vector<uint8_t> span_pieces;  // LASTQ pieces per (kvh, last pair), [hkv][n_last_pairs]
 };
 
@@ -84,6 +90,7 @@ Schedule build_schedule(const Geometry &g, int num_ctas);
 std::vector<uint8_t> serialize(const Schedule &s);
 // Partial-output slots (split-K workspace) and their byte size (g from build_schedule).
 int64_t num_partial_slots(const Geometry &g);
+size_t partial_bytes(const Geometry &g);
 size_t workspace_bytes(const Geometry &g);
 
 }  // namespace ta
