@@ -457,15 +457,15 @@ def main():
             barrier()
             return statistics.median(a.elapsed_time(b) for a, b in evs)
         on, off = [], []
-        for _ in range(3):   # interleaved
-            on.append(step_ms(10))
-            ta.set_pdl(False)
-            off.append(step_ms(10))
-            ta.set_pdl(True)
+        for r in range(8):   # ABBA order: clock drift under the power cap cancels
+            pdl_on = r % 4 in (0, 3)
+            ta.set_pdl(pdl_on)
+            (on if pdl_on else off).append(step_ms(10))
+        ta.set_pdl(True)
         pdl = {"step_ms_pdl": statistics.median(on), "step_ms_no_pdl": statistics.median(off),
                "saved_us": 1e3 * (statistics.median(off) - statistics.median(on)),
                "what": "median step (attention + merge) with the merge launched with / without "
-                       "programmatic dependent launch, interleaved"}
+                       "programmatic dependent launch, 4 + 4 runs of 10 steps in ABBA order"}
 
     fl_layer = kept_flops(c, c.hq)
     fl_rank = kept_flops(c, hq_l)

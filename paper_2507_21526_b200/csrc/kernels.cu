@@ -208,6 +208,12 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_SHORT_BODY  // blocks of <= 80 S columns run a 5-chunk softmax body (see below)
 #define TA_SHORT_BODY 1
 #endif
+#ifndef TA_SHORT_STREAM_ONLY  // the short body only for STREAM items (not DENSE / LASTQ blocks)
+#define TA_SHORT_STREAM_ONLY 0
+#endif
+#ifndef TA_SHORT4  // a third, 4-chunk body for blocks of <= 64 columns (Qwen: P = 36)
+#define TA_SHORT4 0
+#endif
 #ifndef TA_EPI_FMUL2
 #define TA_EPI_FMUL2 0
 #endif
@@ -1204,7 +1210,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ptx::tc_fence_before();
         sm_arrive((kHPR == 2 && hc == 0) ? &p_ready[x] : &p_hi[x]);
         };
-        if (TA_SHORT_BODY && kHPR == 1 && TA_TILE_TRIM == 0 && !TA_SKIP_RAGGED && b.ncols <= 80)
+        const bool short_ok = TA_SHORT_BODY && kHPR == 1 && TA_TILE_TRIM == 0 && !TA_SKIP_RAGGED &&
+                              (!TA_SHORT_STREAM_ONLY || f.kind == kStream);
+        if (TA_SHORT4 && short_ok && b.ncols <= 64)
+          block_body(std::integral_constant<int, 4>{});
+        else if (short_ok && b.ncols <= 80)
           block_body(std::integral_constant<int, 5>{});
         else
           block_body(std::integral_constant<int, kNCol / 16>{});
