@@ -684,6 +684,7 @@ def main():
 
     if rank == 0:
         peak, peak_sus, hbm, src = measured_peaks()
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
         achieved = fl_rank / (attn_ms * 1e-3) / 1e12
         traffic, traffic_src = ncu_traffic() if (args.workload == "C3" and world == 1) else (None, None)
         # compulsory bytes of the layer shard: bf16 Q, O (hq_l heads) and K, V (kv heads)
@@ -717,7 +718,14 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
                          "kernel": "attn_kernel<128> (persistent tcgen05 flash attention)",
-                         "algorithmic_flops_per_launch": fl_rank},
+                         "algorithmic_flops_per_launch": fl_rank,
+                         # the same achieved FLOP/s against the dense bf16 tensor rate at the SM
+                         # clock sampled during this run (148 SMs x 8192 FLOP/clk): how much of
+                         # the gap to `peak` is the power-capped clock rather than the kernel
+                         "peak_at_run_clock": (sms * 8192 * clocks["sm_mhz"] * 1e6 / 1e12
+                                               if clocks.get("sm_mhz") else None),
+                         "frac_at_run_clock": (achieved / (sms * 8192 * clocks["sm_mhz"] * 1e6 / 1e12)
+                                               if clocks.get("sm_mhz") else None)},
             "hbm": hbm_line,
             "cpu_baseline": cpu,
             "e2e": e2e,

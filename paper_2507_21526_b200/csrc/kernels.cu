@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernel_params.h"
@@ -1555,7 +1556,11 @@ cudaError_t launch_attention(const AttnParams &p, int head_dim, int num_ctas, cu
 // GPU, up to 64-128 on an 8-way head shard) spread over the whole GPU.
 template <int D>
 static cudaError_t launch_merge_t(const AttnParams &p, int64_t rows, cudaLaunchConfig_t &cfg) {
-  const int w = p.s_max <= 8 ? 1 : p.s_max <= 16 ? 2 : p.s_max <= 32 ? 4 : 8;
+  static const int forced = [] {  // TA_MERGE_W=1|2|4|8: experiment override
+    const char *e = getenv("TA_MERGE_W");
+    return e ? atoi(e) : 0;
+  }();
+  const int w = forced ? forced : p.s_max <= 8 ? 1 : p.s_max <= 16 ? 2 : p.s_max <= 32 ? 4 : 8;
   const int64_t rpb = 8 / w;
   cfg.gridDim = dim3((unsigned)((rows + rpb - 1) / rpb));
   switch (w) {
