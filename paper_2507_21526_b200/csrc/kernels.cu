@@ -197,6 +197,9 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_EXP_QONCE
 #define TA_EXP_QONCE 0
 #endif
+#ifndef TA_EXP_QKEARLY  // timing probe (wrong results): QK^T(next) issued before PV (chain length)
+#define TA_EXP_QKEARLY 0
+#endif
 #ifndef TA_EXP_NOMASK  // timing only: no kept-column masking (wrong results)
 #define TA_EXP_NOMASK 0
 #endif
@@ -826,6 +829,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           if (j == 0) ++ws_acc[15];  // items
           ++ws_acc[14];              // block pairs
 #endif
+          bool qk_a_done = false;
+          if (TA_EXP_QKEARLY && more) {  // timing probe: QK_A(next) before PV_A (overwrites P)
+            if (last) {
+              ++nitem;
+              WS(0, MMA_WAIT(q_full, nitem & 1u));
+            }
+            WS(2, MMA_WAIT(&kv_full[kslot1], kph1));
+            ptx::tc_fence_after();
+            WS(8, issue_qk(0, kslot1, f1, b1));
+            WS(10, commit(&s_full[0]));
+            qk_a_done = true;
+          }
           if (TA_PV_SPLIT) {
             WS(9, issue_pv(0, vslot, f, b, j > 0, 0));  // keys 0..63 while the softmax finishes 64..127
             WS(4, MMA_WAIT(&p_hi[0], pph[0] ^ 1u));
@@ -838,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           WS(9, issue_pv(0, vslot, f, b, j > 0, 4));
           TRACE_MM(11, j);
           if (last) commit(&o_full[0]);
-          if (more) {
+          if (more && !qk_a_done) {
             if (last) {  // the next item's Q tiles
               ++nitem;
               if (!TA_EXP_QONCE) WS(0, MMA_WAIT(q_full, nitem & 1u));
@@ -861,6 +876,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           TRACE_MM(13, j);
           if (j == 0 && kitem > 0) WS(5, MMA_WAIT(&o_free[1], (kitem - 1) & 1u));  // O_B drained
+          bool qk_b_done = false;
+          if (TA_EXP_QKEARLY && more) {  // timing probe (see tile A)
+            ptx::tc_fence_after();
+            WS(8, issue_qk(1, kslot1, f1, b1));
+            WS(10, commit(&s_full[1]));
+            qk_b_done = true;
+          }
           if (TA_PV_SPLIT) {
             WS(9, issue_pv(1, vslot, f, b, j > 0, 0));  // keys 0..63 while the softmax finishes 64..127
             WS(7, MMA_WAIT(&p_hi[1], pph[1] ^ 1u));
@@ -876,8 +898,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           WS(10, commit(&kv_empty[vslot]));
           seq += 2;
           if (!more) break;
-          WS(8, issue_qk(1, kslot1, f1, b1));
-          WS(10, commit(&s_full[1]));
+          if (!qk_b_done) {
+            WS(8, issue_qk(1, kslot1, f1, b1));
+            WS(10, commit(&s_full[1]));
+          }
           TRACE_MM(15, j);
           WS(10, commit(&kv_empty[kslot1]));
           if (j1 + 1 == f1.nb) commit(q_empty);  // last QK^T of that item issued
@@ -1560,7 +1584,9 @@ static cudaError_t launch_merge_t(const AttnParams &p, int64_t rows, cudaLaunchC
     const char *e = getenv("TA_MERGE_W");
     return e ? atoi(e) : 0;
   }();
-  const int w = forced ? forced : p.s_max <= 8 ? 1 : p.s_max <= 16 ? 2 : p.s_max <= 32 ? 4 : 8;
+  // measured (scripts/merge_w.py): C3 s_max 11: W = 1 12.8 us, 2 15.6, 4 17.0; 8-way C3
+  // s_max 80: W = 8 12.5 us, 4 14.1, 1 24.4; 8-way C2 s_max 38: W = 8 8.4 us, 4 9.7
+  const int w = forced ? forced : p.s_max <= 16 ? 1 : p.s_max <= 24 ? 4 : 8;
   const int64_t rpb = 8 / w;
   cfg.gridDim = dim3((unsigned)((rows + rpb - 1) / rpb));
   switch (w) {

@@ -174,7 +174,8 @@ Schedule build_schedule(const Geometry &g0, int num_ctas) {
   {
     std::vector<std::pair<int64_t, Item>> t;
     for (int c = 0; c < num_ctas; ++c) {
-      const int k = std::min<int>(kTailPerCta, ((int)per[c].size() + 1) / 3);
+      const int k = std::min<int>(std::min<int>(kTailPerCta, ((int)per[c].size() + 1) / kTailDiv),
+                                  (int)per[c].size());
       for (int i = 0; i < k; ++i) {
         const Item it = per[c].back();
         per[c].pop_back();

@@ -48,6 +48,10 @@ constexpr int kMaxCtas = 255;                     // chunk indices are u8 (<= 1 
 #define TA_TAIL_PER_CTA 8
 #endif
 constexpr int kTailPerCta = TA_TAIL_PER_CTA;      // items per CTA moved to the shared tail (at most)
+#ifndef TA_TAIL_DIV  // ... and at most (n + 1) / TA_TAIL_DIV of a CTA's n LPT items
+#define TA_TAIL_DIV 3
+#endif
+constexpr int kTailDiv = TA_TAIL_DIV;
 constexpr size_t kQueueBytes = 256;               // work-queue counter block at the workspace end
 
 struct Geometry {
