@@ -319,12 +319,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Plumbing check on a 1-GPU box only (never for measurements): every rank on cuda:0,
+    # gloo instead of NCCL (NCCL refuses two ranks on one GPU).
+    one_gpu_check = os.environ.get("TA_BENCH_ONE_GPU_CHECK") == "1"
+    if one_gpu_check:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu_check:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2507_21526_b200 import shard
     c = synth.CONFIGS[args.workload]
@@ -402,7 +410,10 @@ def main():
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if one_gpu_check:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
