@@ -103,7 +103,8 @@ typedef struct {
 /* Bytes of device workspace triangle_attn_prefill / dense_attn_prefill need: the split-K
  * partial outputs and their LSE for the Last-rows pass (triangle only) plus a
  * 256-byte block holding the fetch counter of the schedule's shared tail (every call; reset
- * by the call itself on its stream, so concurrent calls must use different workspaces).
+ * inside the call's own kernel -- no separate memset -- so concurrent calls must use
+ * different workspaces; its contents between calls need not be preserved).
  * tri == NULL -> dense.  Returns 0 on invalid arguments. */
 size_t ta_workspace_size(const ta_problem *p, const ta_triangle *tri);
 

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <map>
 #include <atomic>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -18,6 +19,18 @@
 #include "schedule.h"
 
 namespace {
+
+// Launch ids for the in-kernel reset of the tail counter (kernel_params.h `epoch`).
+uint32_t next_epoch() {
+  static std::atomic<uint32_t> counter{0x9e3779b9u ^ (uint32_t)(uintptr_t)&counter ^
+                                       (uint32_t)std::chrono::steady_clock::now().time_since_epoch().count()};
+  uint32_t ep;
+  do {
+    ep = counter.fetch_add(1, std::memory_order_relaxed);
+  } while (ep == 0u);
+  return ep;
+}
+
 
 thread_local std::string g_last_error;
 
@@ -421,11 +434,13 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
     g_trace_buf = tbuf;
   }
 #endif
-  // the shared tail's fetch counter starts at 0 (it lives in the caller's workspace, so calls
-  // on different streams never share it)
-  cudaError_t e = cudaMemsetAsync(prm.queue, 0, sizeof(uint32_t), stream);
-  if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("queue reset: ") + cudaGetErrorString(e));
-  e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
+  // The shared tail's fetch counter (in the caller's workspace, so calls on different
+  // streams never share it) is reset by the kernel itself: CTA 0 zeroes it and publishes
+  // this launch's epoch, which tail fetches wait for (kernel_params.h).  No memset is
+  // enqueued before the launch.  Epochs are distinct for 2^32 launches per process and
+  // start at a per-process salt, so a fresh workspace's leftover bytes do not look current.
+  prm.epoch = next_epoch();
+  cudaError_t e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
   if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
   if (rec.a1) cudaEventRecord(rec.a1, stream);
   if (!dense && ds.g.n_last_pairs > 0) {

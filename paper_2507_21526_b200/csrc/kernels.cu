@@ -512,6 +512,10 @@ constexpr int kOutMulticast = 2;  // + 16-byte multimem stores to the multicast 
 template <int D, int kMode>
 __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant__ AttnParams p) {
   using C = Cfg<D>;
+#ifdef TA_CTA_CLOCK
+  unsigned long long cta_g0;  // globaltimer at kernel entry (before the prologue)
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(cta_g0));
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -667,11 +671,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       // Item source: this CTA's own list, then entries of the shared tail fetched from a
       // global counter (the next one is fetched while the current item loads).
       const uint32_t own0 = p.offsets[blockIdx.x], own1 = p.offsets[blockIdx.x + 1];
+      // Tail counter reset in-kernel (no memset launch before the kernel): CTA 0 zeroes it
+      // and then publishes the launch epoch with a release store.
+      bool queue_ok = false;
+      if (blockIdx.x == 0 && leader) {
+        *reinterpret_cast<volatile uint32_t *>(p.queue) = 0u;
+        ptx::st_release_u32(p.queue + 1, p.epoch);
+        queue_ok = true;
+      }
       const int leader_lane = __ffs(__ballot_sync(0xffffffffu, leader)) - 1;
       auto fetch = [&](uint32_t k) -> int {  // item index of this CTA's k-th item, -1 = none
         if (own0 + k < own1) return (int)(own0 + k);
         uint32_t t = 0;
-        if (leader) t = atomicAdd(p.queue, 1u);
+        if (leader) {
+          // the counter is valid once CTA 0 has published this launch's epoch (normally
+          // long before: a CTA reaches the tail after its own list)
+          while (!queue_ok) {
+            queue_ok = ptx::ld_acquire_u32(p.queue + 1) == p.epoch;
+            if (!queue_ok) __nanosleep(128);
+          }
+          t = atomicAdd(p.queue, 1u);
+        }
         t = __shfl_sync(0xffffffffu, t, leader_lane);
         return t < (uint32_t)p.n_tail ? p.tail0 + (int)t : -1;
       };
@@ -1418,7 +1438,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   // griddepcontrol.wait still orders every read after this grid's completion).
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef TA_CTA_CLOCK
-  if (threadIdx.x == 0) p.trace[blockIdx.x] = (unsigned long long)(clock64() - cta_t0);
+  if (threadIdx.x == 0) {
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    p.trace[blockIdx.x] = (unsigned long long)(clock64() - cta_t0);
+    p.trace[256 + 2 * blockIdx.x] = cta_g0;  // globaltimer (ns) at CTA start / end
+    p.trace[257 + 2 * blockIdx.x] = g1;
+  }
 #endif
   if (warp == kAllocWarp) {
     ptx::tc_fence_after();

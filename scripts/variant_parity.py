@@ -14,7 +14,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     import synth
     from oracle import cref
     out = []
-    for dist in ("iid", "large", "sink", "ones_v"):
+    for dist in os.environ.get("DISTS", "iid,large,sink,ones_v,ramp").split(","):
         q, k, v = synth.make_qkv(32, 8, 4097, 128, 77, dist, 8)
         o = ta.triangle_attn_prefill(q.cuda(), k.cuda(), v.cuda(), sink=8, window=512, last_q=128)
         od = ta.dense_attn_prefill(q.cuda(), k.cuda(), v.cuda())

@@ -73,6 +73,15 @@ def make_qkv(hq: int, hkv: int, n: int, d: int, seed: int, dist: str = "iid", si
         v[:, j, j % d] = 1.0
     elif dist == "ones_v":
         v.fill_(1.0)
+    elif dist == "ramp":
+        # scores that grow along every 384-key period by ~80 log2 units: later key blocks
+        # of a row exceed the first block's max by far more than any lazy-rescale headroom
+        # (exercises the rescale / deferred-max re-run paths; DESIGN reading R15)
+        u = torch.randn(d, generator=g)
+        u = u / u.norm()
+        q = 0.5 * q + 4.0 * u
+        a = 160.0 * (torch.arange(n, dtype=torch.float32) % 384) / 384.0
+        k = 0.5 * k + a[None, :, None] * u
     else:
         raise ValueError(dist)
     return q.to(torch.bfloat16), k.to(torch.bfloat16), v.to(torch.bfloat16)
