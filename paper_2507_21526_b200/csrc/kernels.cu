@@ -197,6 +197,9 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_EXP_QONCE
 #define TA_EXP_QONCE 0
 #endif
+#ifndef TA_COLD_START  // first item: Q and K0 first, the rest of the ring after Q has landed
+#define TA_COLD_START 1
+#endif
 #ifndef TA_EXP_QKEARLY  // timing probe (wrong results): QK^T(next) issued before PV (chain length)
 #define TA_EXP_QKEARLY 0
 #endif
@@ -637,10 +640,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           TRACE_PR(1, nitem);
         }
       };
-      auto load_kv = [&](const ItemInfo &f, int j) {
+      // K (kv = 0) and / or V (kv = 1) of block j, each into the next ring slot
+      auto load_kv = [&](const ItemInfo &f, int j, int kv0 = 0, int kv1 = 2) {
         spin_cycles(TA_DELAY_TMA);
         const Blk b = block_info(f, j);
-        for (int kv = 0; kv < 2; ++kv, ++seq) {
+        for (int kv = kv0; kv < kv1; ++kv, ++seq) {
           uint32_t slot, ph;
           ring_pos(seq, C::kStages, slot, ph);
           WS(1, ptx::mbar_wait_lazy(&kv_empty[slot], ph ^ 1u));
@@ -707,8 +711,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         if (cur < 0) break;
         ItemInfo f;
         item_info(p, p.items[cur], f);
-        load_kv(f, 0);
-        if (!TA_EXP_QONCE || nitem == 0) load_q(f, nitem);
+        if (nitem == 0 && TA_COLD_START) {
+          // Kernel start: every CTA's ring and Q tiles are empty and the data is in HBM, so
+          // the first tile loads of all CTAs form one burst.  Only what the first QK^T needs
+          // (Q, K0) goes out first; V0 and the rest of the ring follow once Q has landed,
+          // which moves the first tensor work forward by the rest of the burst.
+          load_q(f, nitem);
+          load_kv(f, 0, 0, 1);
+          WS(0, ptx::mbar_wait_lazy(q_full, 0u));
+          load_kv(f, 0, 1, 2);
+        } else {
+          load_kv(f, 0);
+          if (!TA_EXP_QONCE || nitem == 0) load_q(f, nitem);
+        }
         // fetch the next entry only now: a tail fetch's atomic round trip overlaps this
         // item's loads instead of delaying them
         next = fetch(nitem + 1);
