@@ -440,6 +440,9 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
   // enqueued before the launch.  Epochs are distinct for 2^32 launches per process and
   // start at a per-process salt, so a fresh workspace's leftover bytes do not look current.
   prm.epoch = next_epoch();
+#ifdef TA_QUEUE_MEMSET
+  cudaMemsetAsync(prm.queue, 0, sizeof(uint32_t), stream);
+#endif
   cudaError_t e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
   if (e != cudaSuccess) return fail(TA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
   if (rec.a1) cudaEventRecord(rec.a1, stream);

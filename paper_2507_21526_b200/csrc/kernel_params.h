@@ -31,9 +31,9 @@ struct alignas(64) AttnParams {
   const uint32_t *offsets;
   const uint8_t *span_pieces;  // LASTQ pieces per (kvh, last pair) = merge chunk counts
   int tail0, n_tail;      // shared tail: items[tail0 .. tail0 + n_tail), fetched dynamically
-  uint32_t *queue;        // [0]: next tail entry to fetch; [1]: epoch of the launch that reset [0]
-  uint32_t epoch;         // this launch's nonzero id: CTA 0 zeroes queue[0], then publishes
-                          // queue[1] = epoch; tail fetches wait for it (no host-side memset)
+  uint32_t *queue;        // 64-bit word {epoch (hi), next tail entry to fetch (lo)}
+  uint32_t epoch;         // this launch's nonzero id: CTA 0 resets the word to {epoch, 0};
+                          // tail tickets carrying another epoch are retried (no host memset)
   int n, hq, group, tile_tokens, pair_tokens;
   int si, sl, last, dense;
   int last_only;     // final-layer mode: the merge writes only rows >= N - last ...

@@ -101,9 +101,16 @@ constexpr int kEpiWarps = TA_EPI_WARPS;
 constexpr bool kEpiLow = TA_EPI_LOW != 0 && kHPR == 1 && kEpiWarps == 4;
 constexpr int kSmWarp0 = kEpiLow ? kEpiWarps : 0;
 constexpr int kEpiWarp0 = kEpiLow ? 0 : kSoftmaxWarps;
-constexpr int kMmaWarp = kSoftmaxWarps + kEpiWarps;
-constexpr int kTmaWarp = kMmaWarp + 1;
-constexpr int kAllocWarp = kMmaWarp + 2;
+// Issuer warps: the four warps after the softmax and epilogue warps.  TA_MMA_SLOT picks the
+// MMA issuer's SM sub-partition (warp % 4): 0 shares SMSP 0 with the epilogue's store-issuing
+// warp; the TMA producer and TMEM allocator take the next slots.
+#ifndef TA_MMA_SLOT
+#define TA_MMA_SLOT 0
+#endif
+constexpr int kIssuer0 = kSoftmaxWarps + kEpiWarps;
+constexpr int kMmaWarp = kIssuer0 + TA_MMA_SLOT;
+constexpr int kTmaWarp = kIssuer0 + (TA_MMA_SLOT + 1) % 4;
+constexpr int kAllocWarp = kIssuer0 + (TA_MMA_SLOT + 2) % 4;
 constexpr int kThreads = 32 * (kSoftmaxWarps + kEpiWarps + 4);
 // 1 (default): no item_empty hand-back.  Slot reuse is safe by the pipeline's own back-
 // pressure: the producer publishes item k+1 only after issuing item k's K/V loads (4-slot
@@ -496,6 +503,17 @@ __device__ __forceinline__ void norm_iv(int &lo, int &hi) {
   }
 }
 
+// Tail ticket that carried another launch's epoch (it reached the queue word before CTA 0's
+// reset): wait and retry until the reset has landed.  Out of line: never taken in practice.
+__device__ __noinline__ unsigned long long stale_ticket_retry(uint32_t *queue, uint32_t epoch) {
+  unsigned long long v;
+  do {
+    __nanosleep(256);
+    v = atomicAdd(reinterpret_cast<unsigned long long *>(queue), 1ull);
+  } while ((v >> 32) != epoch);
+  return v;
+}
+
 // 16-byte store to a multicast (NVLS) address: one egress, every bound GPU receives it.
 __device__ __forceinline__ void mc_st16(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("multimem.st.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
@@ -515,7 +533,7 @@ constexpr int kOutMulticast = 2;  // + 16-byte multimem stores to the multicast 
 template <int D, int kMode>
 __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant__ AttnParams p) {
   using C = Cfg<D>;
-#ifdef TA_CTA_CLOCK
+#if defined(TA_CTA_CLOCK) && defined(TA_GT)
   unsigned long long cta_g0;  // globaltimer at kernel entry (before the prologue)
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(cta_g0));
 #endif
@@ -575,9 +593,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     }
     ptx::fence_mbar_init();
   }
-  // Rows >= G*T of a Q tile are never written by TMA: keep them zero.
-  for (int i = threadIdx.x; i < 2 * C::kQTileBytes / 16; i += kThreads)
-    reinterpret_cast<uint4 *>(sQ)[i] = make_uint4(0, 0, 0, 0);
+  // Rows >= G*T of a Q tile are never written by TMA: keep them zero (only when G*T < 128,
+  // e.g. Qwen's G = 7; a full tile is overwritten by every Q load).
+  if (p.group * p.tile_tokens < kTileRows)
+    for (int i = threadIdx.x; i < 2 * C::kQTileBytes / 16; i += kThreads)
+      reinterpret_cast<uint4 *>(sQ)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == kAllocWarp) {
     ptx::tmem_alloc(tmem_slot, 512);
@@ -610,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   };
 
   // Register split: softmax warpgroups kRegSoftmax, epilogue kRegEpi, issuers kRegOther.
-  if (warp >= kMmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegOther) : "memory");
+  if (warp >= kIssuer0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegOther) : "memory");
   else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegEpi) : "memory");
 
@@ -675,26 +695,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       // Item source: this CTA's own list, then entries of the shared tail fetched from a
       // global counter (the next one is fetched while the current item loads).
       const uint32_t own0 = p.offsets[blockIdx.x], own1 = p.offsets[blockIdx.x + 1];
-      // Tail counter reset in-kernel (no memset launch before the kernel): CTA 0 zeroes it
-      // and then publishes the launch epoch with a release store.
-      bool queue_ok = false;
-      if (blockIdx.x == 0 && leader) {
-        *reinterpret_cast<volatile uint32_t *>(p.queue) = 0u;
-        ptx::st_release_u32(p.queue + 1, p.epoch);
-        queue_ok = true;
-      }
+      // Tail counter reset in-kernel (no memset launch before the kernel): CTA 0 swaps in
+      // {this launch's epoch, count 0} with an atomic at L2.
+#ifndef TA_QUEUE_MEMSET
+      if (blockIdx.x == 0 && leader)
+        atomicExch(reinterpret_cast<unsigned long long *>(p.queue), (unsigned long long)p.epoch << 32);
+#endif
       const int leader_lane = __ffs(__ballot_sync(0xffffffffu, leader)) - 1;
       auto fetch = [&](uint32_t k) -> int {  // item index of this CTA's k-th item, -1 = none
         if (own0 + k < own1) return (int)(own0 + k);
         uint32_t t = 0;
         if (leader) {
-          // the counter is valid once CTA 0 has published this launch's epoch (normally
-          // long before: a CTA reaches the tail after its own list)
-          while (!queue_ok) {
-            queue_ok = ptx::ld_acquire_u32(p.queue + 1) == p.epoch;
-            if (!queue_ok) __nanosleep(128);
-          }
+          // queue word = epoch << 32 | count.  A ticket is valid only if it carries this
+          // launch's epoch, i.e. CTA 0's reset came first (normally long before: a CTA
+          // reaches the tail after its own list); an increment that hit the previous
+          // launch's word is overwritten by the reset and retried.
+#ifdef TA_QUEUE_MEMSET  // (experiment) host memset before the launch, plain 32-bit ticket
           t = atomicAdd(p.queue, 1u);
+#else
+          unsigned long long v = atomicAdd(reinterpret_cast<unsigned long long *>(p.queue), 1ull);
+          if (__builtin_expect((v >> 32) != p.epoch, 0)) v = stale_ticket_retry(p.queue, p.epoch);
+          t = (uint32_t)v;
+#endif
         }
         t = __shfl_sync(0xffffffffu, t, leader_lane);
         return t < (uint32_t)p.n_tail ? p.tail0 + (int)t : -1;
@@ -1454,11 +1476,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef TA_CTA_CLOCK
   if (threadIdx.x == 0) {
+    p.trace[blockIdx.x] = (unsigned long long)(clock64() - cta_t0);
+#ifdef TA_GT  // (+0.8 % cycles: the entry timestamp stays live in warp 0 all kernel long)
     unsigned long long g1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
-    p.trace[blockIdx.x] = (unsigned long long)(clock64() - cta_t0);
     p.trace[256 + 2 * blockIdx.x] = cta_g0;  // globaltimer (ns) at CTA start / end
     p.trace[257 + 2 * blockIdx.x] = g1;
+#endif
   }
 #endif
   if (warp == kAllocWarp) {

@@ -58,13 +58,14 @@ for name in names:
             full = np.zeros(256 + 2 * 148, dtype=np.uint64)
             lib.ta_debug_trace_read(full.ctypes.data, full.nbytes)
             buf = full[:148]
-            g = full[256:].reshape(148, 2).astype(np.int64)
+            g = full[256:].reshape(148, 2).astype(np.int64)  # zeros unless a TA_GT build
             t0 = g[:, 0].min()
             # CTA start skew and end spread (globaltimer, us): launch ramp and tail
             row["cta_start_us_max"] = float((g[:, 0].max() - t0) / 1e3)
             row["cta_end_us_min"] = float((g[:, 1].min() - t0) / 1e3)
             row["cta_end_us_max"] = float((g[:, 1].max() - t0) / 1e3)
-            row["sm_mhz_est"] = float(buf.max() / ((g[:, 1] - g[:, 0])[int(buf.argmax())] / 1e3))
+            span = (g[:, 1] - g[:, 0])[int(buf.argmax())]
+            row["sm_mhz_est"] = float(buf.max() / (span / 1e3)) if span > 0 else None
             row["cta_cycles_max"] = int(buf.max())
             row["cta_cycles_mean"] = float(buf.mean())
             row["cta_cycles_min"] = int(buf.min())
