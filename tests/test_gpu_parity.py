@@ -356,3 +356,37 @@ def test_multi_destination_errors():
     with pytest.raises(ta.TriattnError):
         ta.triangle_attn_prefill_multi(q, k[:1], v[:1], [torch.zeros((4, 63, 128), dtype=torch.bfloat16,
                                                                      device="cuda")], o)
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_poisoned_workspace_tail_queue(dense):
+    """The shared tail's fetch counter is reset inside the kernel (DESIGN 4.5: CTA 0 swaps in
+    {epoch, 0}; tickets of another epoch are retried), so random bytes over the whole
+    workspace -- split-K partials and the queue word -- between calls change nothing: every
+    call is bitwise equal to the first (the schedule's items are computed identically
+    whichever CTA takes them), and the first equals the oracle within tolerance."""
+    hq, hkv, n = 32, 8, 9000  # tens of tail items per launch
+    q, k, v = synth.make_qkv(hq, hkv, n, 128, seed=23)
+    dev = torch.device("cuda")
+    qd, kd, vd = q.to(dev), k.to(dev), v.to(dev)
+
+    def call():
+        o = torch.full_like(qd, float("nan"))
+        if dense:
+            ta.dense_attn_prefill(qd, kd, vd, o)
+        else:
+            ta.triangle_attn_prefill(qd, kd, vd, o, sink=8, window=512, last_q=128)
+        torch.cuda.synchronize()
+        return o
+
+    first = call()
+    g = torch.Generator(device=dev).manual_seed(5)
+    for _ in range(3):
+        for buf in list(ta._ws_cache.values()):
+            buf.copy_(torch.randint(0, 256, buf.shape, dtype=torch.uint8, device=dev, generator=g))
+        torch.cuda.synchronize()
+        assert torch.equal(call(), first)
+    rows = np.r_[0:40, 4000:4040, n - 200:n]  # sink-only, streaming and last rows
+    ref, _, _ = cref.attention(q, k, v, 8, 512, 128, dense, rows=rows)
+    err = np.abs(first.float().cpu().numpy()[:, rows, :] - ref)
+    assert err.max() <= MAX_ABS and err.mean() <= MEAN_ABS
