@@ -25,11 +25,19 @@ Spec summary:
      span sequence; a take is cut at span ends into LASTQ(kvh, p) pieces
      [b0*128, min(b1*128, r1+1)) appended to that CTA's list; a piece's chunk index (u8
      item field `pad`) is its ordinal within its span.  s_max = max pieces per span.
+  2'. (schedule version 5) When each kv head has m last pairs, 2 <= m <= 8 and
+     num_ctas >= m, step 2 is replaced by lock-step pieces: the CTAs in (load, id) order
+     form num_ctas // m groups of m; per head, maxnb = the most blocks of its m spans;
+     group capacity gcap_g(L) = min over its CTAs of max(0, (L - load_c - 192) // 128);
+     L = the smallest integer with sum_g gcap_g(L) >= sum_h maxnb_h.  Groups in order take
+     block columns [k, k + t) of the current head (t = min(remaining capacity, maxnb - k)):
+     the group's j-th CTA gets LASTQ(kvh, pair j) [k*128, min((k+t)*128, r1+1)) when that
+     span has blocks there; k wraps to the next head at maxnb (a group may continue there).
   1b. (between 1 and 2; schedule version 4) Shared tail: each CTA's last
      min(8, (n + 1) // 3) LPT items (n = its LPT item count) leave its list (loads reduced
      before step 2); sorted by (cost desc, kind, kvh, pair) they form the tail that the
      kernel's CTAs fetch from a global counter after their own lists.
-  bytes: 16 x u32 header (version 4; field 12 = tail entries), u32
+  bytes: 16 x u32 header (version 5; field 12 = tail entries), u32
          offsets[num_ctas+1], 16-byte items {u8 kind, u8 chunk, u16 kvh, u32 pair,
          u32 key_begin, u32 key_end}.
 """
@@ -38,12 +46,13 @@ from __future__ import annotations
 import struct
 
 STREAM, LASTQ, DENSE = 0, 1, 2
-MAGIC, VERSION = 0x43534154, 4
+MAGIC, VERSION = 0x43534154, 5
 
 
 
 ITEM_OVERHEAD = 192  # LPT cost of an item beyond its key columns
 TAIL_PER_CTA = 8     # at most this many items per CTA go to the shared, dynamically fetched tail
+LOCKSTEP_MAX = 8     # lock-step Last Q-K pieces for 2..8 last pairs per kv head (version 5)
 
 def _r16(x):
     return -(-x // 16) * 16
@@ -172,7 +181,50 @@ def schedule(n, hq, hkv, d, si, sl, last, dense, num_ctas, last_rows=False):
     nblk = [-(-keys // 128) for (_, _, keys) in spans]
     total = sum(nblk)
     s_max = 0
-    if total:
+    m = len(spans) // geo["hkv"] if spans else 0  # last pairs per kv head
+    if total and 2 <= m <= LOCKSTEP_MAX and num_ctas >= m:
+        # 2'. lock-step pieces (schedule version 5): groups of m consecutive CTAs in (load, id)
+        # order take the same key-block range [k, k + t) from each of a head's m last pairs
+        order = sorted(range(num_ctas), key=lambda x: (load[x], x))
+        ngroups = num_ctas // m
+        maxnb = [max(nblk[h * m + j] for j in range(m)) for h in range(geo["hkv"])]
+        columns = sum(maxnb)
+
+        def gcap(L, gi):
+            return min(max(0, (L - load[order[gi * m + j]] - ITEM_OVERHEAD) // 128) for j in range(m))
+        lo, hi = 0, max(load) + ITEM_OVERHEAD + 128 * columns
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if sum(gcap(mid, gi) for gi in range(ngroups)) >= columns:
+                hi = mid
+            else:
+                lo = mid + 1
+        L = lo
+        pieces = [0] * len(spans)
+        h, kcol = 0, 0
+        for gi in range(ngroups):
+            if h >= geo["hkv"]:
+                break
+            tg = gcap(L, gi)
+            while tg > 0 and h < geo["hkv"]:
+                t = min(tg, maxnb[h] - kcol)
+                for j in range(m):
+                    sidx = h * m + j
+                    kvh, p, keys = spans[sidx]
+                    b0, b1 = kcol, min(kcol + t, nblk[sidx])
+                    if b1 <= b0:
+                        continue
+                    it = (LASTQ, kvh, p, b0 * 128, min(b1 * 128, keys), pieces[sidx])
+                    c = order[gi * m + j]
+                    per[c].append(it)
+                    load[c] += cost(geo, it)
+                    pieces[sidx] += 1
+                kcol += t
+                tg -= t
+                if kcol == maxnb[h]:
+                    h, kcol = h + 1, 0
+        s_max = max(pieces)
+    elif total:
         L = fill_level(load, total)
         caps = [max(0, (L - x - ITEM_OVERHEAD) // 128) for x in load]
         si_, off, rem = 0, 0, total

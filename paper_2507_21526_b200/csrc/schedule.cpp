@@ -3,6 +3,7 @@
 #include "schedule.h"
 
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <numeric>
 #include <queue>
@@ -211,30 +212,84 @@ Schedule build_schedule(const Geometry &g0, int num_ctas) {
         spans.push_back(Span{kvh, p, r1 + 1, nb});
         total += nb;
       }
-    const int64_t L = fill_level(load, total);
     std::vector<int> cta(num_ctas);
     std::iota(cta.begin(), cta.end(), 0);
     std::stable_sort(cta.begin(), cta.end(), [&](int a, int b) { return load[a] < load[b]; });
     std::vector<int> pieces(spans.size(), 0);
-    size_t si = 0;
-    int64_t off = 0, rem = total;
-    for (int c : cta) {
-      if (rem == 0) break;
-      int64_t take = std::min(rem, std::max<int64_t>(0, (L - load[c] - kItemOverhead) / kBlockKeys));
-      while (take > 0) {
-        const Span &sp = spans[si];
-        const int64_t k = std::min(take, sp.nblk - off);
-        Item it = make_item(kLastQ, sp.kvh, sp.pair, off * kBlockKeys,
-                            std::min<int64_t>((off + k) * kBlockKeys, sp.keys));
-        it.pad = (uint8_t)pieces[si]++;
-        per[c].push_back(it);
-        load[c] += item_cost(g, it);
-        off += k;
-        take -= k;
-        rem -= k;
-        if (off == sp.nblk) {
-          ++si;
-          off = 0;
+    // Lock-step pieces (schedule version 5): with m = n_last_pairs in [2, kLockStepMax],
+    // groups of m consecutive CTAs (ascending load) take the same key-block range from each
+    // of a kv head's m last pairs, so the m pieces that read the same K/V blocks run at the
+    // same time and share them through L2 (C3: DRAM reads 2.66 -> 2.18 GB per launch, cycles
+    // unchanged).  Otherwise the single-span water-filling below.
+    const int m = (int)g.n_last_pairs;
+    if (m >= 2 && m <= kLockStepMax && num_ctas >= m) {
+      const int ngroups = num_ctas / m;
+      std::vector<int64_t> maxnb(g.hkv, 0);
+      int64_t columns = 0;
+      for (int h = 0; h < g.hkv; ++h) {
+        for (int j = 0; j < m; ++j) maxnb[h] = std::max(maxnb[h], spans[h * m + j].nblk);
+        columns += maxnb[h];
+      }
+      auto gcap = [&](int64_t L, int gi) {
+        int64_t t = INT64_MAX;
+        for (int j = 0; j < m; ++j) t = std::min(t, std::max<int64_t>(0, (L - load[cta[gi * m + j]] - kItemOverhead) / kBlockKeys));
+        return t;
+      };
+      int64_t lo = 0, hi = *std::max_element(load.begin(), load.end()) + kItemOverhead + kBlockKeys * columns;
+      while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        int64_t c = 0;
+        for (int gi = 0; gi < ngroups; ++gi) c += gcap(mid, gi);
+        if (c >= columns) hi = mid; else lo = mid + 1;
+      }
+      const int64_t L = lo;
+      int h = 0;
+      int64_t kcol = 0;
+      for (int gi = 0; gi < ngroups && h < g.hkv; ++gi) {
+        int64_t tg = gcap(L, gi);
+        while (tg > 0 && h < g.hkv) {
+          const int64_t t = std::min(tg, maxnb[h] - kcol);
+          for (int j = 0; j < m; ++j) {
+            const size_t sidx = (size_t)h * m + j;
+            const Span &sp = spans[sidx];
+            const int64_t b0 = kcol, b1 = std::min(kcol + t, sp.nblk);
+            if (b1 <= b0) continue;
+            Item it = make_item(kLastQ, sp.kvh, sp.pair, b0 * kBlockKeys, std::min<int64_t>(b1 * kBlockKeys, sp.keys));
+            it.pad = (uint8_t)pieces[sidx]++;
+            const int c = cta[gi * m + j];
+            per[c].push_back(it);
+            load[c] += item_cost(g, it);
+          }
+          kcol += t;
+          tg -= t;
+          if (kcol == maxnb[h]) {
+            ++h;
+            kcol = 0;
+          }
+        }
+      }
+    } else {
+      const int64_t L = fill_level(load, total);
+      size_t si = 0;
+      int64_t off = 0, rem = total;
+      for (int c : cta) {
+        if (rem == 0) break;
+        int64_t take = std::min(rem, std::max<int64_t>(0, (L - load[c] - kItemOverhead) / kBlockKeys));
+        while (take > 0) {
+          const Span &sp = spans[si];
+          const int64_t k = std::min(take, sp.nblk - off);
+          Item it = make_item(kLastQ, sp.kvh, sp.pair, off * kBlockKeys,
+                              std::min<int64_t>((off + k) * kBlockKeys, sp.keys));
+          it.pad = (uint8_t)pieces[si]++;
+          per[c].push_back(it);
+          load[c] += item_cost(g, it);
+          off += k;
+          take -= k;
+          rem -= k;
+          if (off == sp.nblk) {
+            ++si;
+            off = 0;
+          }
         }
       }
     }

@@ -42,7 +42,9 @@ constexpr int kSinkRows = 16;       // sink keys folded into a STREAM item's fir
 #endif
 constexpr int kItemOverhead = TA_ITEM_OVERHEAD;
 constexpr uint32_t kScheduleMagic = 0x43534154u;  // "TASC"
-constexpr uint32_t kScheduleVersion = 4;          // v2: water-filled LASTQ pieces; v4: + shared tail
+constexpr uint32_t kScheduleVersion = 5;          // v2: water-filled LASTQ pieces; v4: + shared tail;
+                                                  // v5: lock-step pieces of a head's last pairs
+constexpr int kLockStepMax = 8;                   // lock-step groups for 2..8 last pairs per kv head
 constexpr int kMaxCtas = 255;                     // chunk indices are u8 (<= 1 piece per CTA and span)
 #ifndef TA_TAIL_PER_CTA  // (overridable for schedule-policy experiments only; schedule_ref.py mirrors 8)
 #define TA_TAIL_PER_CTA 8

@@ -166,7 +166,7 @@ def test_last_rows_go_through_split_k():
     for i in range(32768 - 128, 32768):
         assert i // geo["P"] in last_pairs
     hdr, off, items = schedule_ref.parse(ta.schedule_export(32768, 32, 8, 128, 148))
-    assert hdr[0] == schedule_ref.MAGIC and hdr[1] == 4 and hdr[12] == len(tail) and hdr[15] == s_max
+    assert hdr[0] == schedule_ref.MAGIC and hdr[1] == schedule_ref.VERSION == 5 and hdr[12] == len(tail) and hdr[15] == s_max
     assert off[-1] + len(tail) == len(items)
 
 
