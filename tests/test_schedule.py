@@ -219,3 +219,24 @@ def test_streamingmix_has_no_split_k():
     hdr, off, items = schedule_ref.parse(ta.schedule_export(4096, 32, 8, 128, 148, 8, 512, 0))
     assert items and all(it[0] == schedule_ref.STREAM for it in items)
     assert ta.workspace_size(4096, 32, 8, 128, 8, 512, 0) == 256   # the work-queue block only
+
+
+@pytest.mark.parametrize("n,hq,hkv", [(131072, 32, 8), (32768, 4, 1), (131072, 28, 4), (65536, 3, 1)])
+def test_lockstep_pieces_share_key_ranges(n, hq, hkv):
+    """Schedule v5 (DESIGN 4.4 3'): a kv head's m last pairs are cut at the same key blocks,
+    and the m pieces of each range sit on m different CTAs of one group (adjacent in the
+    ascending-load order), so they run together and read each K/V block once from HBM."""
+    geo, _, _, per, _, _ = schedule_ref.schedule(n, hq, hkv, 128, 8, 512, 128, False, 148)
+    m = geo["pairs"] - geo["p_last0"]
+    assert 2 <= m <= schedule_ref.LOCKSTEP_MAX
+    where = {}
+    for c, lst in enumerate(per):
+        for it in lst:
+            if it[0] == schedule_ref.LASTQ:
+                where.setdefault((it[1], it[3] // 128), []).append((it[2], c))
+    for (kvh, blk), lst in where.items():
+        pairs = sorted(p for p, _ in lst)
+        ctas = {c for _, c in lst}
+        # every last pair whose span reaches this block has a piece starting here, each on its own CTA
+        assert len(ctas) == len(lst) and len(set(pairs)) == len(pairs)
+        assert len(lst) >= m - 1
