@@ -435,12 +435,13 @@ ta_status run(const ta_problem *p, const ta_triangle *tri, Mode mode, int32_t la
   }
 #endif
   // The shared tail's fetch counter (in the caller's workspace, so calls on different
-  // streams never share it) is reset by the kernel itself: CTA 0 zeroes it and publishes
-  // this launch's epoch, which tail fetches wait for (kernel_params.h).  No memset is
-  // enqueued before the launch.  Epochs are distinct for 2^32 launches per process and
-  // start at a per-process salt, so a fresh workspace's leftover bytes do not look current.
+  // streams never share it) is reset by the kernel itself: CTA 0 swaps the 64-bit word to
+  // {this launch's epoch, 0}, and a ticket is valid only if it carries that epoch
+  // (kernel_params.h).  No memset is enqueued before the launch.  Epochs are
+  // distinct for 2^32 launches per process and start at a per-process salt, so a fresh
+  // workspace's leftover bytes do not look current.
   prm.epoch = next_epoch();
-#ifdef TA_QUEUE_MEMSET
+#ifdef TA_QUEUE_MEMSET  // (experiment) the round-2 memset reset, 32-bit tickets
   cudaMemsetAsync(prm.queue, 0, sizeof(uint32_t), stream);
 #endif
   cudaError_t e = ta::launch_attention(prm, g.d, ds.num_ctas, stream);
