@@ -196,6 +196,11 @@ constexpr int kPolyPairs = TA_POLY_MASK;
 #ifndef TA_EARLY_K
 #define TA_EARLY_K 0
 #endif
+#ifndef TA_SPLIT  // 16-column chunks of P handed to the MMA first (p_ready); even, <= 8
+#define TA_SPLIT 4
+#endif
+constexpr int kSplit = TA_SPLIT;
+static_assert(kSplit % 2 == 0 && kSplit >= 2 && kSplit <= 8, "P hand-off split");
 // Timing-only experiments (wrong results; never in a shipped build): skip the epilogue's
 // work (NOEPI) or load Q only for a CTA's first item (QONCE).
 #ifndef TA_EXP_NOEPI
@@ -804,8 +809,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
       };
       // O_x += P_x V_slot; P_x (bf16) lives in the S_x columns; V MN-major (d contiguous).
-      // k-steps [s0, s0 + 4) of the block (keys 16 s .. 16 s + 15)
-      auto issue_pv = [&](int x, uint32_t vslot, const ItemInfo &fq, const Blk &b, bool acc, int s0) {
+      // k-steps [s0, s1) of the block (keys 16 s .. 16 s + 15)
+      auto issue_pv = [&](int x, uint32_t vslot, const ItemInfo &fq, const Blk &b, bool acc, int s0, int s1) {
         if (!leader) return;
         const uint64_t b0 = dkv_mn + (uint64_t)((vslot * C::kSlotBytes) >> 4);
         const int ksteps = tile_ncols(fq, b, x, p.tile_tokens) / 16;
@@ -813,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         // P of keys [64h, 64h + 64) sits in TMEM columns [64h, 64h + 32) of S_x when two
         // threads share a row (each writes over its own S columns), else in [0, 64).
 #pragma unroll
-        for (int s = s0; s < s0 + 4; ++s)
+        for (int s = s0; s < s1; ++s)
           if (s < ksteps)
             ptx::mma_ts(tm + 256u + 128u * x,
                         pcol + (s / (8 / kHPR)) * 64 + (s % (8 / kHPR)) * 8,
@@ -899,15 +904,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             qk_a_done = true;
           }
           if (TA_PV_SPLIT) {
-            WS(9, issue_pv(0, vslot, f, b, j > 0, 0));  // keys 0..63 while the softmax finishes 64..127
+            WS(9, issue_pv(0, vslot, f, b, j > 0, 0, kSplit));  // keys 0..16 kSplit - 1 while the softmax finishes the rest
             WS(4, MMA_WAIT(&p_hi[0], pph[0] ^ 1u));
           } else {
             MMA_WAIT(&p_hi[0], pph[0]);
             pph[0] ^= 1u;
           }
           ptx::tc_fence_after();
-          if (!TA_PV_SPLIT) issue_pv(0, vslot, f, b, j > 0, 0);
-          WS(9, issue_pv(0, vslot, f, b, j > 0, 4));
+          if (!TA_PV_SPLIT) issue_pv(0, vslot, f, b, j > 0, 0, kSplit);
+          WS(9, issue_pv(0, vslot, f, b, j > 0, kSplit, 8));
           TRACE_MM(11, j);
           if (last) commit(&o_full[0]);
           if (more && !qk_a_done) {
@@ -941,15 +946,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             qk_b_done = true;
           }
           if (TA_PV_SPLIT) {
-            WS(9, issue_pv(1, vslot, f, b, j > 0, 0));  // keys 0..63 while the softmax finishes 64..127
+            WS(9, issue_pv(1, vslot, f, b, j > 0, 0, kSplit));  // keys 0..16 kSplit - 1 while the softmax finishes the rest
             WS(7, MMA_WAIT(&p_hi[1], pph[1] ^ 1u));
           } else {
             MMA_WAIT(&p_hi[1], pph[1]);
             pph[1] ^= 1u;
           }
           ptx::tc_fence_after();
-          if (!TA_PV_SPLIT) issue_pv(1, vslot, f, b, j > 0, 0);
-          WS(9, issue_pv(1, vslot, f, b, j > 0, 4));
+          if (!TA_PV_SPLIT) issue_pv(1, vslot, f, b, j > 0, 0, kSplit);
+          WS(9, issue_pv(1, vslot, f, b, j > 0, kSplit, 8));
           TRACE_MM(14, j);
           if (last) commit(&o_full[1]);
           WS(10, commit(&kv_empty[vslot]));
@@ -1192,7 +1197,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 #pragma unroll
         for (int c = 0; c < kNCol / 16; ++c) {
           if (c >= nch) {
-            if (kHPR == 1 && c == 3 && TA_PV_SPLIT) {  // keep the p_ready hand-off when the block is short
+            if (kHPR == 1 && c == kSplit - 1 && TA_PV_SPLIT) {  // keep the p_ready hand-off when the block is short
               ptx::tmem_wait_st();
               ptx::tc_fence_before();
               sm_arrive(&p_ready[x]);
@@ -1259,7 +1264,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             ptx::tmem_st16(tS + (c - 1) * 8, pkw);
           else if (c == kCh - 1)  // odd chunk count (short body): the last chunk alone
             ptx::tmem_st8(tS + c * 8, pk);
-          if (kHPR == 1 && c == 3 && TA_PV_SPLIT) {
+          if (kHPR == 1 && c == kSplit - 1 && TA_PV_SPLIT) {
             // keys 0..63 of P are in TMEM: the MMA can start PV on them right away
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
