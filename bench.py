@@ -612,36 +612,41 @@ def main():
             del q2, k2, v2, o2
 
     # ---- strong-scaling proxy on 1 GPU: the per-rank kernel at the 2/4/8-way kv-head
-    # shard shapes of C3 and C2; efficiency = (full-layer ms / P) / shard ms.
+    # shard shapes of C3, C2 and Qwen 128K; efficiency = (full-layer ms / P) / shard ms.
     shard_pts = None
     if not args.no_points and world == 1:
         shard_pts = []
-        for name in ("C3", "C2"):
+        for name in ("C3", "C2", "C4b"):   # Llama 128K / 32K, Qwen2.5-7B 128K
             cc = synth.CONFIGS[name]
             full = None
             for P in (1, 2, 4, 8):
-                g = cc.hq // cc.hkv
-                q1, k1, v1 = (t.to(dev) for t in synth.make_qkv(g * cc.hkv // P, cc.hkv // P, cc.n,
-                                                                   cc.d, seed=100 + P))
-                o1 = torch.empty_like(q1)
-                fn = lambda: ta.triangle_attn_prefill(q1, k1, v1, o1, sink=cc.si, window=cc.sl,
-                                                      last_q=cc.last)
-                for _ in range(3):
-                    fn()
-                barrier()
-                ta.profile_begin()
-                for _ in range(10):
-                    flush.zero_()
-                    fn()
-                barrier()
-                pr = ta.profile_end()
-                kms = (pr["attn_ms"] + pr["merge_ms"]) / 10
+                # per-rank shapes of shard.head_plan (kv-head shards; Qwen at 8 ranks splits
+                # each kv head's 7 q heads 3 + 4): time each distinct shape, the step is the max
+                shapes = sorted({(q1_ - q0_, kv1_ - kv0_) for kv0_, kv1_, q0_, q1_ in
+                                 shard.head_plan(cc.hq, cc.hkv, P)})
+                kms = 0.0
+                for hq_r, hkv_r in shapes:
+                    q1, k1, v1 = (t.to(dev) for t in synth.make_qkv(hq_r, hkv_r, cc.n, cc.d, seed=100 + P))
+                    o1 = torch.empty_like(q1)
+                    fn = lambda: ta.triangle_attn_prefill(q1, k1, v1, o1, sink=cc.si, window=cc.sl,
+                                                          last_q=cc.last)
+                    for _ in range(3):
+                        fn()
+                    barrier()
+                    ta.profile_begin()
+                    for _ in range(10):
+                        flush.zero_()
+                        fn()
+                    barrier()
+                    pr = ta.profile_end()
+                    kms = max(kms, (pr["attn_ms"] + pr["merge_ms"]) / 10)
+                    del q1, k1, v1, o1
                 if P == 1:
                     full = kms
-                shard_pts.append({"workload": name, "ranks": P, "hq_per_rank": g * cc.hkv // P,
+                shard_pts.append({"workload": name, "ranks": P,
+                                  "hq_per_rank": "/".join(str(h) for h, _ in shapes),
                                   "kernel_ms_per_rank": kms,
                                   "strong_scaling_eff": full / (P * kms)})
-                del q1, k1, v1, o1
 
     # ---- NEXT rows on 1 GPU (extra keys): final-layer last rows (f1), StreamingMix (f3),
     # and the C5 attention stack per rank of an 8-way kv-head shard (16 dense + 16 triangle).
