@@ -1502,6 +1502,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 // (chunks strided over the warps; W grows with the chunk count so that rows with many
 // chunks -- small head shards, where ck is small -- still spread over the whole GPU),
 // combined through shared memory.  Launched with PDL (griddepcontrol.wait first).
+#ifndef TA_MERGE_U  // chunks whose loads a merge warp issues before using them
+#define TA_MERGE_U 4
+#endif
 template <int D, int W>
 __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ AttnParams p) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1541,8 +1544,8 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Attn
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   float wsum = 0.f;
-  // Four chunks per step with all their loads issued first (latency-bound loop).
-  constexpr int U = 4;
+  // U chunks per step with all their loads issued first (latency-bound loop).
+  constexpr int U = TA_MERGE_U;
   for (int c0 = sub; c0 < nch; c0 += U * W) {
     float lcs[U], vv[U][E];
 #pragma unroll
